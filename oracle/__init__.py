@@ -1,0 +1,269 @@
+"""CPU oracle for the uniqueness embedding-gradient exchange (arXiv 1810.10045 Sec. 3.1).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_1810_10045_b200`` never imports it, and
+the two share no code.
+
+The arithmetic lives in ``oracle.c`` (plain loops, fp64 accumulation, one
+rounding to fp32).  This module only marshals numpy arrays through ctypes and
+strings the paper's seven steps together in the paper's order:
+
+1. local unique J^          -> ``unique_local``
+2. local reduction Delta^   -> ``reduce_local``
+3. AllGather of J -> I      -> ``allgather_ids``
+4. global unique I^ + maps  -> ``unique_global``, ``remap``
+5. expand to M_i, zeros     -> ``scatter_expand``
+6. AllReduce -> M^          -> ``allreduce_sum``
+7. row update of E          -> ``update_rows``
+
+``sync_unique`` runs the seven steps for G simulated ranks; ``sync_dense``
+is the baseline all-gather exchange.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain -O2, no fast-math: fp64 stays IEEE)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11",
+                               "-fno-fast-math", "-ffp-contract=off", _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            i64 = ctypes.c_int64
+            lib.oracle_unique_local.restype = i64
+            lib.oracle_unique_local.argtypes = [P, i64, P, P, P]
+            lib.oracle_reduce_local.restype = None
+            lib.oracle_reduce_local.argtypes = [P, i64, i64, P, i64, P]
+            lib.oracle_allgather_ids.restype = None
+            lib.oracle_allgather_ids.argtypes = [P, P, ctypes.c_int, P]
+            lib.oracle_unique_global.restype = i64
+            lib.oracle_unique_global.argtypes = [P, i64, P, P]
+            lib.oracle_remap.restype = None
+            lib.oracle_remap.argtypes = [P, i64, P, i64, P, i64, P, P]
+            lib.oracle_scatter_expand.restype = None
+            lib.oracle_scatter_expand.argtypes = [P, i64, i64, P, i64, P]
+            lib.oracle_allreduce_sum.restype = None
+            lib.oracle_allreduce_sum.argtypes = [P, ctypes.c_int, i64, P]
+            lib.oracle_update_rows.restype = None
+            lib.oracle_update_rows.argtypes = [P, i64, P, i64, P, ctypes.c_double]
+            lib.oracle_sync_dense.restype = None
+            lib.oracle_sync_dense.argtypes = [P, P, i64, i64, ctypes.c_int, P, P, P,
+                                              ctypes.c_double]
+            lib.oracle_type_gradient.restype = i64
+            lib.oracle_type_gradient.argtypes = [P, P, P, ctypes.c_int, i64,
+                                                 ctypes.c_uint32, P, P]
+            _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr_array(arrs):
+    return (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+
+
+# --------------------------------------------------------------------------- steps
+
+def unique_local(J):
+    """Step 1. Returns (J^ ascending uint32, counts int32, inverse int32)."""
+    lib = _load()
+    J = _u32(J)
+    K = J.size
+    uniq = np.empty(K, np.uint32)
+    counts = np.empty(K, np.int32)
+    inverse = np.empty(K, np.int32)
+    U = lib.oracle_unique_local(_p(J), K, _p(uniq), _p(counts), _p(inverse))
+    return uniq[:U].copy(), counts[:U].copy(), inverse
+
+
+def reduce_local(delta, inverse, U):
+    """Step 2. fp64 Delta^ (U x D), ascending-position sums."""
+    lib = _load()
+    delta = _f32(delta)
+    K, D = delta.shape
+    inverse = np.ascontiguousarray(inverse, dtype=np.int32)
+    out = np.empty((U, D), np.float64)
+    lib.oracle_reduce_local(_p(delta), K, D, _p(inverse), U, _p(out))
+    return out
+
+
+def allgather_ids(J_list):
+    """Step 3. Rank-ordered concatenation I of every rank's J."""
+    lib = _load()
+    Js = [_u32(j) for j in J_list]
+    Ks = np.array([j.size for j in Js], np.int64)
+    I = np.empty(int(Ks.sum()), np.uint32)
+    lib.oracle_allgather_ids(_ptr_array(Js), _p(Ks), len(Js), _p(I))
+    return I
+
+
+def unique_global(I):
+    """Step 4. Returns (I^ ascending uint32, global counts int32)."""
+    lib = _load()
+    I = _u32(I)
+    n = I.size
+    Ihat = np.empty(n, np.uint32)
+    gcounts = np.empty(n, np.int32)
+    U = lib.oracle_unique_global(_p(I), n, _p(Ihat), _p(gcounts))
+    return Ihat[:U].copy(), gcounts[:U].copy()
+
+
+def remap(Jhat, Ihat, inverse):
+    """Step 4 maps: l2g (J^ -> I^) and slot (J -> I^)."""
+    lib = _load()
+    Jhat = _u32(Jhat)
+    Ihat = _u32(Ihat)
+    inverse = np.ascontiguousarray(inverse, dtype=np.int32)
+    l2g = np.empty(Jhat.size, np.int32)
+    slot = np.empty(inverse.size, np.int32)
+    lib.oracle_remap(_p(Jhat), Jhat.size, _p(Ihat), Ihat.size, _p(inverse),
+                     inverse.size, _p(l2g), _p(slot))
+    return l2g, slot
+
+
+def scatter_expand(dhat, l2g, Ug):
+    """Step 5. fp64 M_i (Ug x D): Delta^ rows at l2g, zeros elsewhere."""
+    lib = _load()
+    dhat = np.ascontiguousarray(dhat, dtype=np.float64)
+    Ui, D = dhat.shape
+    l2g = np.ascontiguousarray(l2g, dtype=np.int32)
+    M = np.empty((Ug, D), np.float64)
+    lib.oracle_scatter_expand(_p(dhat), Ui, D, _p(l2g), Ug, _p(M))
+    return M
+
+
+def allreduce_sum(M_list):
+    """Step 6. Rank-ordered fp64 sum of the M_i."""
+    lib = _load()
+    Ms = [np.ascontiguousarray(m, dtype=np.float64) for m in M_list]
+    out = np.empty_like(Ms[0])
+    lib.oracle_allreduce_sum(_ptr_array(Ms), len(Ms), out.size, _p(out))
+    return out
+
+
+def update_rows(E, Ihat, Mhat64, lr):
+    """Step 7. In place: E[I^[r]] = round32(E[I^[r]] - lr * M^64[r])."""
+    lib = _load()
+    assert E.dtype == np.float32 and E.flags.c_contiguous
+    Ihat = _u32(Ihat)
+    Mhat64 = np.ascontiguousarray(Mhat64, dtype=np.float64)
+    D = E.shape[1]
+    lib.oracle_update_rows(_p(E), D, _p(Ihat), Ihat.size, _p(Mhat64), float(lr))
+    return E
+
+
+# ---------------------------------------------------------------- composites
+
+def sync_unique(J_list, delta_list, E, lr):
+    """The uniqueness exchange, steps 1-7 for G simulated ranks.
+
+    ``E`` (V x D fp32) is updated in place (one replica stands for all G:
+    they receive the same M^ and I^).  Returns a dict of every intermediate.
+    """
+    G = len(J_list)
+    ranks = []
+    for g in range(G):                                   # steps 1, 2
+        Jhat, counts, inverse = unique_local(J_list[g])
+        dhat = reduce_local(delta_list[g], inverse, Jhat.size)
+        ranks.append(dict(Jhat=Jhat, counts=counts, inverse=inverse, dhat=dhat))
+    I = allgather_ids(J_list)                            # step 3
+    Ihat, gcounts = unique_global(I)                     # step 4
+    Ug = Ihat.size
+    Ms = []
+    for r in ranks:
+        r["l2g"], r["slot"] = remap(r["Jhat"], Ihat, r["inverse"])
+        Ms.append(scatter_expand(r["dhat"], r["l2g"], Ug))   # step 5
+    Mhat64 = allreduce_sum(Ms)                           # step 6
+    update_rows(E, Ihat, Mhat64, lr)                     # step 7
+    return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M=Ms,
+                Mhat64=Mhat64, Mhat=Mhat64.astype(np.float32), E=E)
+
+
+def sync_dense(J_list, delta_list, E, lr):
+    """Baseline all-gather exchange; E (V x D fp32) updated in place."""
+    lib = _load()
+    assert E.dtype == np.float32 and E.flags.c_contiguous
+    V, D = E.shape
+    Js = [_u32(j) for j in J_list]
+    Ds = [_f32(d) for d in delta_list]
+    Ks = np.array([j.size for j in Js], np.int64)
+    E64 = np.empty((V, D), np.float64)
+    lib.oracle_sync_dense(_p(E), _p(E64), V, D, len(Js), _ptr_array(Js), _ptr_array(Ds),
+                          _p(Ks), float(lr))
+    return E
+
+
+def type_gradient(J_list, delta_list, w):
+    """One row of M^ from the definition: fp64 sum of every Delta row of
+    word ``w`` over all ranks, plus the summation-error scale A = sum |Delta|.
+    Returns (row fp64[D], A fp64[D], number of tokens)."""
+    lib = _load()
+    Js = [_u32(j) for j in J_list]
+    Ds = [_f32(d) for d in delta_list]
+    Ks = np.array([j.size for j in Js], np.int64)
+    D = Ds[0].shape[1]
+    out = np.empty(D, np.float64)
+    absout = np.empty(D, np.float64)
+    n = lib.oracle_type_gradient(_ptr_array(Js), _ptr_array(Ds), _p(Ks), len(Js), D,
+                                 int(w), _p(out), _p(absout))
+    return out, absout, int(n)
+
+
+def abs_scale(J_list, delta_list, Ihat):
+    """A[r,:] = sum of |Delta| over every token of word I^[r] (fp64) -- the
+    summation-error scale of the SIGNED-mode metric.
+    Same loop as steps 1-6 applied to |Delta|."""
+    absd = [np.abs(_f32(d)) for d in delta_list]
+    Ms = []
+    for J, a in zip(J_list, absd):
+        Jhat, _, inverse = unique_local(J)
+        dh = reduce_local(a, inverse, Jhat.size)
+        l2g, _ = remap(Jhat, Ihat, inverse)
+        Ms.append(scatter_expand(dh, l2g, len(Ihat)))
+    return allreduce_sum(Ms)
+
+
+def complexity_plan(G, K, D, alpha, elem_bytes=4, index_bytes=4):
+    """Sec. 3.1 complexity: dense Theta(GKD) bytes vs
+    unique Theta(GK + U_g D) with U_g estimated as (GK)^alpha."""
+    baseline = G * K * D * elem_bytes
+    ug = (G * K) ** alpha
+    grad = ug * D * elem_bytes
+    idx = G * K * index_bytes
+    return dict(baseline_bytes=baseline, u_g_estimate=ug, unique_grad_bytes=grad,
+                unique_index_bytes=idx, saving_factor=baseline / (idx + grad),
+                saving_factor_grad_only=baseline / grad)

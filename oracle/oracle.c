@@ -1,0 +1,215 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the uniqueness
+ * embedding-gradient exchange of Patwary et al., "Language Modeling at Scale"
+ * (arXiv 1810.10045), Sec. 3.1.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1810_10045_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant with the CUDA path.
+ *
+ * Citations: "P:n" = PAPER.md line n (Sec. 3.1 enumerate);
+ * "S:n" = SPEC.md line n.  Every floating-point accumulation is fp64; the
+ * single rounding to fp32 happens where the function says so (DESIGN.md
+ * reading R5).  No blocking, fusion or reordering beyond the paper's steps.
+ *
+ * Parity status: every function below is pinned by tests/test_oracle_*.py
+ * (goldens, library cross-checks, brute force, invariants); see the
+ * "Pins" table in DESIGN.md.  No function is "parity unpinned".
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* qsort comparator: a library primitive serves as the sort of step 1/4. */
+static int cmp_u32(const void* a, const void* b) {
+  uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* lower_bound: first index i in sorted a[0..n) with a[i] >= key. */
+static int64_t lower_bound_u32(const uint32_t* a, int64_t n, uint32_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+/*
+ * Step 1: "compute the vector J^, which holds the word indices of
+ * only unique words in its input sequence" -- J^ = sorted(set(J)) (ascending,
+ * DESIGN.md reading R2), counts[u] = #{p : J[p] = J^[u]},
+ * inverse[p] = lower_bound(J^, J[p]) ("mapping from an entry in J to ...").
+ * uniq/counts need capacity K; inverse has K entries.  Returns U_i.
+ */
+int64_t oracle_unique_local(const uint32_t* J, int64_t K, uint32_t* uniq,
+                            int32_t* counts, int32_t* inverse) {
+  if (K <= 0) return 0;
+  uint32_t* tmp = (uint32_t*)malloc((size_t)K * sizeof(uint32_t));
+  memcpy(tmp, J, (size_t)K * sizeof(uint32_t));
+  qsort(tmp, (size_t)K, sizeof(uint32_t), cmp_u32);
+  int64_t U = 0;
+  for (int64_t i = 0; i < K; ++i)
+    if (i == 0 || tmp[i] != tmp[i - 1]) uniq[U++] = tmp[i];
+  free(tmp);
+  for (int64_t u = 0; u < U; ++u) counts[u] = 0;
+  for (int64_t p = 0; p < K; ++p) {
+    int64_t u = lower_bound_u32(uniq, U, J[p]);
+    inverse[p] = (int32_t)u;
+    counts[u] += 1;
+  }
+  return U;
+}
+
+/*
+ * Step 2: "a local reduction of the gradient vectors, so that the
+ * gradient vectors corresponding to the same words are accumulated into a
+ * single vector" -- dhat[u,:] = sum_{p : inverse[p] = u} delta[p,:], fp64,
+ * ascending p.  dhat is U x D, overwritten.
+ */
+void oracle_reduce_local(const float* delta, int64_t K, int64_t D,
+                         const int32_t* inverse, int64_t U, double* dhat) {
+  for (int64_t i = 0; i < U * D; ++i) dhat[i] = 0.0;
+  for (int64_t p = 0; p < K; ++p) {
+    double* row = dhat + (int64_t)inverse[p] * D;
+    const float* src = delta + p * D;
+    for (int64_t d = 0; d < D; ++d) row[d] += (double)src[d];
+  }
+}
+
+/*
+ * Step 3: AllGather over the J vectors of all G GPUs; I is their
+ * rank-ordered concatenation (reading R1: the text's J, not J^).
+ * Simulated here by copying rank g's K_g ids to offset sum_{h<g} K_h.
+ */
+void oracle_allgather_ids(const uint32_t* const* J, const int64_t* K, int G,
+                          uint32_t* I) {
+  int64_t off = 0;
+  for (int g = 0; g < G; ++g) {
+    memcpy(I + off, J[g], (size_t)K[g] * sizeof(uint32_t));
+    off += K[g];
+  }
+}
+
+/*
+ * Step 4: "a local filter operation over the G x K indices
+ * (vector I) to extract all unique word indices to produce vector I^", "totally
+ * ordered" -> ascending (R2).  gcounts[r] = #{q : I[q] = I^[r]} (global type
+ * counts).  Returns U_g.  Ihat/gcounts need capacity n.
+ */
+int64_t oracle_unique_global(const uint32_t* I, int64_t n, uint32_t* Ihat,
+                             int32_t* gcounts) {
+  if (n <= 0) return 0;
+  uint32_t* tmp = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+  memcpy(tmp, I, (size_t)n * sizeof(uint32_t));
+  qsort(tmp, (size_t)n, sizeof(uint32_t), cmp_u32);
+  int64_t U = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (i == 0 || tmp[i] != tmp[i - 1]) Ihat[U++] = tmp[i];
+  free(tmp);
+  if (gcounts) {
+    for (int64_t r = 0; r < U; ++r) gcounts[r] = 0;
+    for (int64_t q = 0; q < n; ++q) gcounts[lower_bound_u32(Ihat, U, I[q])] += 1;
+  }
+  return U;
+}
+
+/*
+ * Step 4, the maps: "a mapping from an entry in J to the corresponding
+ * entry in I^ and transitively from J^ to I^".
+ *   l2g[u]  = lower_bound(I^, J^[u])            (J^ -> I^)
+ *   slot[p] = l2g[inverse[p]]                   (J  -> I^, transitively)
+ */
+void oracle_remap(const uint32_t* Jhat, int64_t Ui, const uint32_t* Ihat,
+                  int64_t Ug, const int32_t* inverse, int64_t K, int32_t* l2g,
+                  int32_t* slot) {
+  for (int64_t u = 0; u < Ui; ++u) l2g[u] = (int32_t)lower_bound_u32(Ihat, Ug, Jhat[u]);
+  if (slot)
+    for (int64_t p = 0; p < K; ++p) slot[p] = l2g[inverse[p]];
+}
+
+/*
+ * Step 5: "expand the Delta^_i matrix ... from a U_i x D matrix
+ * into a U_g x D matrix via a local scatter operation.  The non existing
+ * entries are filled with zeros" -- M[l2g[u],:] = dhat[u,:], every other row
+ * exactly 0 (R4).  M is Ug x D fp64, overwritten.
+ */
+void oracle_scatter_expand(const double* dhat, int64_t Ui, int64_t D,
+                           const int32_t* l2g, int64_t Ug, double* M) {
+  for (int64_t i = 0; i < Ug * D; ++i) M[i] = 0.0;
+  for (int64_t u = 0; u < Ui; ++u)
+    memcpy(M + (int64_t)l2g[u] * D, dhat + u * D, (size_t)D * sizeof(double));
+}
+
+/*
+ * Step 6: AllReduce over all M_i -> M^ = sum_i M_i, summed in rank
+ * order, fp64.  Mhat has n entries, overwritten.
+ */
+void oracle_allreduce_sum(const double* const* M, int G, int64_t n, double* Mhat) {
+  for (int64_t i = 0; i < n; ++i) Mhat[i] = 0.0;
+  for (int g = 0; g < G; ++g)
+    for (int64_t i = 0; i < n; ++i) Mhat[i] += M[g][i];
+}
+
+/*
+ * Step 7 (no duplicates P:433-435): "Update the local embedding matrix
+ * with the values in M^ using I^ to map index in M^ with row in E" -- plain
+ * SGD on the raw sum (R3): E[I^[r],:] = round32(E[I^[r],:] - lr * M^[r,:]),
+ * evaluated in fp64 and rounded once (R5).  E is V x D fp32, in place.
+ */
+void oracle_update_rows(float* E, int64_t D, const uint32_t* Ihat, int64_t Ug,
+                        const double* Mhat, double lr) {
+  for (int64_t r = 0; r < Ug; ++r) {
+    float* row = E + (int64_t)Ihat[r] * D;
+    for (int64_t d = 0; d < D; ++d)
+      row[d] = (float)((double)row[d] - lr * Mhat[r * D + d]);
+  }
+}
+
+/*
+ * Baseline dense exchange: AllGather all (J, Delta)
+ * pairs and apply every one of the G*K row updates in rank-then-position
+ * order: E64 = E0; E64[J_g[p],:] -= lr * Delta_g[p,:] (fp64); E = round32(E64)
+ * (an untouched row is E0 exactly, so rounding it back is the identity).
+ * E64 is a caller-provided V x D fp64 scratch.  E is V x D fp32, in place.
+ */
+void oracle_sync_dense(float* E, double* E64, int64_t V, int64_t D, int G,
+                       const uint32_t* const* J, const float* const* delta,
+                       const int64_t* K, double lr) {
+  for (int64_t i = 0; i < V * D; ++i) E64[i] = (double)E[i];
+  for (int g = 0; g < G; ++g)
+    for (int64_t p = 0; p < K[g]; ++p) {
+      double* row = E64 + (int64_t)J[g][p] * D;
+      const float* src = delta[g] + p * D;
+      for (int64_t d = 0; d < D; ++d) row[d] -= lr * (double)src[d];
+    }
+  for (int64_t i = 0; i < V * D; ++i) E[i] = (float)E64[i];
+}
+
+/*
+ * Per-type conservation, by definition ("the rows corresponding to the
+ * same word accumulate"): out[:] = sum over all ranks g and positions p with
+ * J_g[p] == w of Delta_g[p,:], fp64, rank-then-position order.  This is one
+ * row of M^ computed from first principles; the full-size GPU parity test
+ * samples rows with it.  Returns the number of contributing tokens.  absout
+ * (optional) receives sum |Delta_g[p,:]| (the summation-error scale A).
+ */
+int64_t oracle_type_gradient(const uint32_t* const* J, const float* const* delta,
+                             const int64_t* K, int G, int64_t D, uint32_t w,
+                             double* out, double* absout) {
+  int64_t n = 0;
+  for (int64_t d = 0; d < D; ++d) { out[d] = 0.0; if (absout) absout[d] = 0.0; }
+  for (int g = 0; g < G; ++g)
+    for (int64_t p = 0; p < K[g]; ++p)
+      if (J[g][p] == w) {
+        const float* src = delta[g] + p * D;
+        for (int64_t d = 0; d < D; ++d) {
+          out[d] += (double)src[d];
+          if (absout) absout[d] += src[d] < 0 ? -(double)src[d] : (double)src[d];
+        }
+        ++n;
+      }
+  return n;
+}
