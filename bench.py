@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the uniqueness embedding-gradient exchange (arXiv 1810.10045 Sec. 3.1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1b] [--impl lmscale|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = the whole hot path (S1 dedup, S2 ID all-gather, S3 global unique,
+S4 scatter-add, S5 all-reduce, S6 row update) over one synthetic batch of K
+tokens per GPU, inputs resident in HBM.  Weak scaling: every rank owns its own
+K tokens.  Prints ONE JSON line on rank 0 (metric/unit from BASELINE.json):
+value = whole-job tokens/s = N*K / (max over ranks of the device-timed step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "emb-grad sync µs/step & tokens/s at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="1b")
+    ap.add_argument("--mode", default="signed", choices=["int", "pos", "signed"])
+    ap.add_argument("--s", type=float, default=None, help="Zipf exponent override")
+    ap.add_argument("--impl", default="lmscale", choices=["lmscale", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------- clocks sampler
+
+class Clocks:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                mask = int(parts[2], 16)
+            except ValueError:
+                continue
+            for bit, name in self.REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------- CPU oracle legs
+
+def oracle_sample(cfg, G, mode, seconds):
+    """Time the CPU oracle (as it stands, single-threaded C) on a bounded sample
+    of the workload: whole G-rank steps over the config's shapes, repeated until
+    ~`seconds` of CPU work.  Returns (tokens/s, sample description, steps)."""
+    import oracle
+    import synth
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    Dl = [synth.grad_values(cfg.K, cfg.D, mode, rank=g).numpy() for g in range(G)]
+    E = np.zeros((cfg.V, cfg.D), np.float32)   # values do not change the oracle's work
+    lr = synth.default_lr(mode)
+    oracle.sync_unique(J, Dl, E, lr)           # build + warm
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        oracle.sync_unique(J, Dl, E, lr)
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt >= seconds or n >= 1000:
+            break
+    tps = n * G * cfg.K / dt
+    desc = (f"{n} full oracle steps of workload {cfg.name} (G={G} simulated ranks x K={cfg.K} "
+            f"tokens, D={cfg.D}) in {dt:.1f}s; single-threaded C, fp64 accumulation")
+    return tps, desc, n, dt
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    import synth  # noqa: F401
+    per_step = max(1.0, min(20.0, 90.0 / max(1, args.steps + args.warmup)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        tps, desc, n, dt = oracle_sample(cfg, world, args.mode, per_step)
+        if i >= args.warmup:
+            times.append(tps)
+    v = statistics.median(times)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * world * cfg.K / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(cfg, args, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line, args)
+
+
+def config_dict(cfg, args, world):
+    return {"workload": cfg.name, "V": cfg.V, "K_per_gpu": cfg.K, "D": cfg.D, "zipf_s": cfg.s,
+            "G": world, "value_mode": args.mode, "global_tokens": world * cfg.K,
+            "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)"}
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(s + "\n")
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    import torch
+    import torch.distributed as dist
+    import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.CONFIGS[args.config]
+    if args.s is not None:
+        cfg = cfg.with_(s=args.s)
+    cfg = cfg.with_(G=world)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    from paper_1810_10045_b200 import lmscale
+    from paper_1810_10045_b200.distributed import make_context, max_over_ranks
+
+    # ---- inputs resident in HBM (seeded, per rank)
+    J = synth.ids_for(cfg, rank)
+    ids = torch.from_numpy(J.view(np.int32)).to(dev)
+    grad = synth.grad_values(cfg.K, cfg.D, args.mode, rank=rank, device=dev)
+    table = synth.table_values(cfg.V, cfg.D, args.mode, device=dev)
+    lr = synth.default_lr(args.mode)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+
+    if world > 1:
+        ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+    else:
+        ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, device=local, flags=lmscale.FLAG_TIMING)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps, warmup, collect=None):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        for i in range(steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            fn()
+            ev[i][1].record(stream)
+            if collect:
+                collect()
+        barrier()
+        ms = [a.elapsed_time(b) for a, b in ev]
+        return ms
+
+    # ---- the unique exchange (S1-S6)
+    phase = {k: [] for k in ("us_dedup", "us_gather", "us_merge", "us_scatter", "us_allreduce",
+                             "us_update", "us_total")}
+    info = {}
+    launches = [0]
+
+    def step():
+        sg = ctx.step(ids, grad, table, lr)
+        info["ug"] = sg.num_unique
+
+    def collect():
+        st = ctx.stats()
+        for k in phase:
+            phase[k].append(st[k])
+        launches[0] += st["kernels_last_call"]
+        info["u_local"] = st["u_local"]
+
+    clk = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
+                 if "CUDA_VISIBLE_DEVICES" in os.environ else local)
+    clk.start()
+    ms = timed(step, args.steps, args.warmup, collect)
+    clocks = clk.stop()
+    total_ms = max_over_ranks(sum(ms), dev)
+    ms_step = total_ms / args.steps
+    tokens = world * cfg.K
+    value = tokens / (ms_step * 1e-3)
+    ug = info["ug"]
+    sync_launches = launches[0]
+
+    # per-phase device times (median over timed steps), max over ranks
+    ph = {k: max_over_ranks(statistics.median(v), dev) for k, v in phase.items() if v}
+    hbm_peak, peak_kind = peaks()
+    scatter_bytes = 4 * cfg.K * cfg.D + 4 * ug * cfg.D
+    update_bytes = 12 * ug * cfg.D
+    scatter_us = ph["us_scatter"]
+    roof = {"kernel": "k_scatter (S4 segmented scatter-add)", "bound": "hbm",
+            "achieved": scatter_bytes / (scatter_us * 1e-6) / 1e9, "peak": hbm_peak,
+            "unit": "GB/s", "peak_kind": peak_kind,
+            "bytes_per_launch": scatter_bytes, "us_per_launch": scatter_us}
+    roof["frac"] = roof["achieved"] / hbm_peak
+    roof["traffic"] = ncu_traffic(cfg.name)
+    upd = {"kernel": "k_update (S6 row update)", "achieved": update_bytes /
+           (ph["us_update"] * 1e-6) / 1e9, "bytes_per_launch": update_bytes,
+           "us_per_launch": ph["us_update"]}
+    upd["frac"] = upd["achieved"] / hbm_peak
+
+    # ---- dense comparison path (S0), same inputs, separate table copy
+    dense = None
+    if not args.no_dense:
+        try:
+            table_d = table.clone()
+            dms = timed(lambda: ctx.sync_dense(ids, grad, table_d, lr), args.steps,
+                        min(args.warmup, 3))
+            dense_ms = max_over_ranks(sum(dms), dev) / args.steps
+            del table_d
+            ratio_model = (world * cfg.K * cfg.D) / (world * cfg.K + ug * cfg.D)
+            dense = {"ms_per_step": dense_ms, "tokens_per_s": tokens / (dense_ms * 1e-3),
+                     "speedup_unique_vs_dense": dense_ms / ms_step,
+                     "paper_ratio_GKD_over_GK_plus_UD": ratio_model,
+                     "gate_0.8x": 0.8 * ratio_model}
+        except Exception as e:  # pragma: no cover
+            dense = {"error": str(e)[:200]}
+
+    # ---- e2e: host (pinned) buffers through the C ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        ids_h = torch.from_numpy(J.view(np.int32)).pin_memory()
+        grad_h = grad.cpu().pin_memory()
+        out_h = torch.empty(world * cfg.K, dtype=torch.int32).pin_memory()
+        ug_box = [0]
+
+        def hstep():
+            ug_box[0] = ctx.train_step_host(ids_h, grad_h, table, lr, out_h)
+
+        ems = timed(hstep, max(3, args.steps // 2), min(args.warmup, 3))
+        e_ms = max_over_ranks(sum(ems), dev) / len(ems)
+        e2e = {"value": tokens / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": 4 * cfg.K + 4 * cfg.K * cfg.D,
+               "d2h_bytes_per_step": 4 * ug_box[0],
+               "api": "lmscale_train_step_host (pinned host ids+grad -> S1..S6 -> I^ to host)"}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tps, desc, n, dt = oracle_sample(cfg, 1, args.mode, args.cpu_seconds)
+        cpu = {"value": tps, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+               "host_cores_available": host_cores()}
+
+    if rank == 0:
+        eu = synth.expected_unique(cfg.V, cfg.s, world * cfg.K)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "us_per_step": 1e3 * ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Zipf ids, "
+                "counter-hash fp32 gradients/table; no datasets)",
+                "config": config_dict(cfg, args, world),
+                "U_local": info.get("u_local"), "U_global": ug, "E_U_global_closed_form": eu,
+                "phases_us_median": ph, "roofline": roof, "roofline_update": upd,
+                "dense_baseline": dense, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+                "gpu_launches": sync_launches, "gpu_launches_per_step": sync_launches / args.steps,
+                "library": lmscale.version()}
+        emit(line, args)
+    ctx.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ncu_traffic(workload):
+    """dram read+write bytes per launch of k_scatter from the committed ncu
+    --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("k_scatter")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

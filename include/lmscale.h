@@ -1,0 +1,228 @@
+/*
+ * lmscale.h -- C ABI of the B200-native uniqueness embedding-gradient
+ * exchange (Patwary et al., "Language Modeling at Scale", arXiv 1810.10045,
+ * Sec. 3.1).
+ *
+ * Problem statement: G data-parallel GPUs; GPU g
+ * holds K token word-indices J_g (uint32) and their K x D fp32 embedding
+ * gradient rows Delta_g; every GPU holds the same |V| x D fp32 embedding table
+ * E.  The exchange replaces the Theta(G K D) all-gather of (J, Delta) pairs
+ * with
+ *   S1  local unique  J -> J^ (+ counts, inverse)                (step 1)
+ *   S2  all-gather of J -> I (G K ids)                            (step 3)
+ *   S3  global unique I -> I^ (ascending), U_g, J^ -> I^ map     (step 4)
+ *   S4  segmented scatter-add Delta -> M_g (U_g x D, zero rows)  (steps 2+5)
+ *   S5  all-reduce M_g -> M^                                      (step 6)
+ *   S6  duplicate-free row update E[I^[r]] -= lr * M^[r]          (step 7)
+ *
+ * Conventions (all functions):
+ *  - Pointers are DEVICE pointers on the context's device unless a parameter
+ *    says "host".  `stream` is a cudaStream_t passed as void* (NULL = the
+ *    legacy default stream); every call is stream-ordered on it.
+ *  - The caller owns ids / grad / table.  The context owns all scratch, sized
+ *    at init from (vocab, max_tokens, dim, world); no call allocates except
+ *    the first lmscale_sync_dense_baseline / lmscale_train_step_host (their
+ *    staging buffers).
+ *  - Ids are uint32 word indices; an id >= vocab is an error
+ *    (LMSCALE_ERR_ID_RANGE), detected on the device and reported at the next
+ *    host synchronisation point of the call that reports it (below).  Kernels
+ *    never access memory out of bounds for such ids; outputs of a call that
+ *    returned an error are unspecified.
+ *  - Row-major layouts: grad is k x dim, table is vocab x dim, rows are
+ *    contiguous with stride dim floats.  dim % 4 == 0 with 16-byte aligned
+ *    pointers takes the 128-bit vector path; any dim >= 1 is accepted.
+ *  - Collective calls (lmscale_sync_embedding_grad, lmscale_sync_dense_baseline,
+ *    lmscale_train_step_host with world > 1) must be made by every rank in the
+ *    same order with the same k (the ID all-gather is fixed-size).  world == 1
+ *    makes no NCCL call.
+ *  - Errors are status codes; nothing is thrown across the ABI.  One context
+ *    per (process, GPU); a context is not thread-safe.
+ *  - Numerics: lr multiplies the raw sum (plain SGD, reading R3);
+ *    pass lr / G for averaging.  Accumulation is fp32.
+ */
+#ifndef LMSCALE_H
+#define LMSCALE_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LMSCALE_API __attribute__((visibility("default")))
+#else
+#define LMSCALE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lmscale_ctx lmscale_ctx; /* opaque, one per rank */
+
+typedef enum {
+  LMSCALE_OK = 0,
+  LMSCALE_ERR_INVALID_ARG = 1, /* null / misaligned pointer, k < 1 or k > max_tokens, bad config, wrong call order */
+  LMSCALE_ERR_ID_RANGE = 2,    /* some id >= vocab */
+  LMSCALE_ERR_CUDA = 3,        /* CUDA runtime error (message: lmscale_last_error) */
+  LMSCALE_ERR_NCCL = 4,        /* NCCL error or asynchronous communicator error */
+  LMSCALE_ERR_OOM = 5,         /* workspace allocation failed */
+  LMSCALE_ERR_UNSUPPORTED = 6  /* e.g. a collective call on a LMSCALE_FLAG_NO_COMM context */
+} lmscale_status;
+
+/* Context flags. */
+#define LMSCALE_FLAG_NO_COMM 1u /* no NCCL communicator: staged calls only (test emulation of G ranks) */
+#define LMSCALE_FLAG_TIMING 2u  /* record CUDA events around each phase; lmscale_get_stats reports them */
+
+typedef struct {
+  int64_t vocab;      /* |V| >= 1 */
+  int64_t max_tokens; /* K capacity per rank, >= 1 */
+  int64_t dim;        /* D >= 1 */
+  int32_t world;      /* G >= 1 */
+  int32_t rank;       /* 0 <= rank < world */
+  int32_t device;     /* CUDA device ordinal of this rank */
+  uint32_t flags;     /* LMSCALE_FLAG_* */
+} lmscale_config;
+
+/* The synchronised sparse gradient: a borrowed view into the context's
+ * workspace, valid until the next call on the same context that runs S1-S5. */
+typedef struct {
+  const uint32_t* ids; /* device, I^ ascending, num_unique entries */
+  float* rows;         /* device, num_unique x dim row-major: M^ after a collective sync,
+                          this rank's M_g after lmscale_scatter_expand */
+  int64_t num_unique;  /* host value U_g */
+} lmscale_sparse_grad;
+
+typedef struct {
+  int64_t u_local;  /* U_i of the last S1 */
+  int64_t u_global; /* U_g of the last S3 */
+  /* per-phase device time of the last collective sync, microseconds (FLAG_TIMING; else -1) */
+  double us_dedup, us_gather, us_merge, us_scatter, us_allreduce, us_update, us_total;
+  /* per-step byte accounting of the last sync (SURVEY Sec. 8(d) algorithmic bytes) */
+  int64_t bytes_ids_gathered;  /* 4 (G-1) K ingress */
+  int64_t bytes_grad_allreduce;/* 4 U_g D payload */
+  int64_t bytes_scatter;       /* 4 K D read + 4 U_g D written */
+  int64_t bytes_update;        /* 12 U_g D */
+  int64_t workspace_bytes;     /* device bytes owned by the context */
+  int32_t kernels_last_call;   /* kernels this library launched in the last call */
+  int32_t kernels_total_lo;    /* running count of launched kernels (low 31 bits) */
+} lmscale_stats;
+
+/* ------------------------------------------------------------------ setup */
+
+/* Rank 0 creates the NCCL unique id (128 host bytes) that every rank passes
+ * to lmscale_init; the caller distributes it (e.g. a torch.distributed
+ * broadcast).  Not needed when world == 1 or FLAG_NO_COMM. */
+LMSCALE_API lmscale_status lmscale_get_nccl_id(uint8_t out_id[128] /* host */);
+
+/* Create a context: cudaSetDevice(cfg->device), ncclCommInitRank when
+ * world > 1 and !FLAG_NO_COMM, and allocate the workspace (about
+ * 4*world*max_tokens + 4*min(world*max_tokens, vocab)*dim + 40*max_tokens +
+ * vocab/2 bytes).  *out receives the context, or NULL on error. */
+LMSCALE_API lmscale_status lmscale_init(const lmscale_config* cfg /* host */,
+                            const uint8_t* nccl_id /* host, 128 bytes, or NULL */,
+                            lmscale_ctx** out /* host */);
+
+/* Free the workspace and the communicator (after a device synchronise). */
+LMSCALE_API void lmscale_destroy(lmscale_ctx* ctx);
+
+/* ------------------------------------------------------- staged operations
+ * These are the per-rank steps of P:402-422 with no communication.  They are
+ * what the collective call below runs between its two NCCL calls, and they let
+ * a test emulate G ranks with G NO_COMM contexts on one GPU. */
+
+/* S1, step 1: J^ = sorted distinct ids (ascending, reading R2),
+ * counts[u] = #{p : ids[p] = J^[u]}, inverse[p] = index of ids[p] in J^.
+ * uniq_out / counts_out need capacity k, inverse_out k entries; each may be
+ * NULL (results stay in the workspace).  *num_unique_out (device int64, may be
+ * NULL) receives U_i.  Errors: INVALID_ARG; ID_RANGE is reported by the next
+ * lmscale_get_sparse_grad / collective call. */
+LMSCALE_API lmscale_status lmscale_unique(lmscale_ctx* ctx, const uint32_t* ids, int64_t k,
+                              uint32_t* uniq_out, int32_t* counts_out,
+                              int32_t* inverse_out, int64_t* num_unique_out,
+                              void* stream);
+
+/* S3, step 4 over a caller-provided gathered id vector I (n ids,
+ * n <= world * max_tokens): I^ = sorted distinct(I), U_g = |I^|, and the map
+ * l2g[u] = position of J^[u] in I^ for the J^ of the last lmscale_unique on
+ * this context. */
+LMSCALE_API lmscale_status lmscale_global_unique(lmscale_ctx* ctx, const uint32_t* gathered,
+                                     int64_t n, void* stream);
+
+/* S4, steps 2+5: M_g[l2g[u]] = sum of grad rows of J^[u]
+ * (segmented fp32 sum, deterministic order), every other of the U_g rows is
+ * exactly 0.  grad is the k x dim gradient belonging to the ids of the last
+ * lmscale_unique (same k).  Requires lmscale_unique then lmscale_global_unique. */
+LMSCALE_API lmscale_status lmscale_scatter_expand(lmscale_ctx* ctx, const float* grad, int64_t k,
+                                      void* stream);
+
+/* Synchronise `stream` and return the view of I^ / M and U_g.  Returns
+ * ID_RANGE if any id seen since the last S1 was >= vocab. */
+LMSCALE_API lmscale_status lmscale_get_sparse_grad(lmscale_ctx* ctx, lmscale_sparse_grad* out /* host */,
+                                       void* stream);
+
+/* Debug/parity views of the last S1/S3 maps (device pointers into the
+ * workspace; synchronises `stream`).  Any out pointer may be NULL. */
+LMSCALE_API lmscale_status lmscale_get_local_maps(lmscale_ctx* ctx, const uint32_t** uniq,
+                                      const int32_t** counts, const int32_t** inverse,
+                                      const int32_t** l2g, int64_t* num_unique_local /* host */,
+                                      void* stream);
+
+/* ------------------------------------------------------ collective path */
+
+/* S1-S5: the whole uniqueness exchange of one step.  ids: k
+ * uint32, grad: k x dim fp32.  On return out->ids / out->rows hold I^ and the
+ * all-reduced M^ (identical on every rank) and out->num_unique = U_g (host).
+ * The call blocks the host until U_g is known (one 16-byte device->host read,
+ * hidden behind S4), because NCCL takes its element count from the host.
+ * world == 1: no NCCL, out->rows = M_0.  Errors: INVALID_ARG, ID_RANGE (all
+ * ranks see it: I is identical everywhere; no all-reduce is issued), CUDA,
+ * NCCL, UNSUPPORTED (NO_COMM context). */
+LMSCALE_API lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids,
+                                           const float* grad, int64_t k,
+                                           lmscale_sparse_grad* out /* host */,
+                                           void* stream);
+
+/* S6, step 7 (no duplicates P:433-435): for r < sg->num_unique,
+ * table[sg->ids[r], :] = table[sg->ids[r], :] - lr * sg->rows[r, :]
+ * (one fused multiply-add per element, rows disjoint, no atomics).  sg is a
+ * view returned by this context (or any device I^/rows pair with the
+ * documented layout).  table: vocab x dim, in place. */
+LMSCALE_API lmscale_status lmscale_apply_sparse_update(lmscale_ctx* ctx, float* table,
+                                           const lmscale_sparse_grad* sg /* host */,
+                                           float lr, void* stream);
+
+/* S0, the comparison path: all-gather ids and the k x dim grad
+ * rows of every rank (Theta(G K D) bytes), then apply all G*k row updates
+ * table[I[q]] -= lr * Delta_all[q] with 128-bit vector atomics (the paper's
+ * "rows under update are locked").  Collective.  First call allocates the
+ * 4*world*max_tokens*dim byte gather buffer. */
+LMSCALE_API lmscale_status lmscale_sync_dense_baseline(lmscale_ctx* ctx, const uint32_t* ids,
+                                           const float* grad, int64_t k, float* table,
+                                           float lr, void* stream);
+
+/* The dense atomic scatter alone (staged dense path): table[ids[q]] -= lr *
+ * grad[q] for q < n.  n <= world * max_tokens. */
+LMSCALE_API lmscale_status lmscale_dense_apply(lmscale_ctx* ctx, const uint32_t* ids, const float* grad,
+                                   int64_t n, float* table, float lr, void* stream);
+
+/* One end-to-end step from HOST buffers: copy ids (k uint32) and grad (k x dim
+ * fp32) host->device (pinned memory recommended), run S1-S6 on `table`
+ * (device), copy I^ back to ids_out (host, capacity world*k) and U_g to
+ * *num_unique_out (host).  Synchronises `stream` before returning.
+ * Collective when world > 1. */
+LMSCALE_API lmscale_status lmscale_train_step_host(lmscale_ctx* ctx, const uint32_t* ids_host,
+                                       const float* grad_host, int64_t k, float* table,
+                                       float lr, uint32_t* ids_out_host,
+                                       int64_t* num_unique_out, void* stream);
+
+/* ---------------------------------------------------------------- misc */
+
+LMSCALE_API lmscale_status lmscale_get_stats(const lmscale_ctx* ctx, lmscale_stats* out /* host */);
+LMSCALE_API const char* lmscale_status_string(lmscale_status s);
+/* Last detailed error message of this context (static storage inside ctx). */
+LMSCALE_API const char* lmscale_last_error(const lmscale_ctx* ctx);
+/* Library version string, e.g. "lmscale 0.1 sm_100a". */
+LMSCALE_API const char* lmscale_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMSCALE_H */

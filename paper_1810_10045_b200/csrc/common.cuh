@@ -1,0 +1,116 @@
+// common.cuh -- device helpers shared by the lmscale kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lms {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Decoupled look-back publication (gpu scope, release / acquire).
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Look-back words: bits 31..30 = flag (1 aggregate, 2 inclusive prefix), 29..0 = count.
+constexpr uint32_t LB_AGG = 1u << 30;
+constexpr uint32_t LB_INC = 2u << 30;
+constexpr uint32_t LB_MASK = (1u << 30) - 1u;
+
+// 128-bit streaming loads/stores.  Gradient rows are read exactly once
+// (no L1 allocation); outputs are written once.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_cg(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_v4(float4* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float4* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024,
+// multiple of 32).  `warp_tot` is shared scratch of >= 32 words.  Returns the
+// exclusive prefix; *total receives the block sum (all threads).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot,
+                                                    uint32_t* total) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t t = lane < nwarps ? warp_tot[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULL, t, o);
+      if (lane >= (unsigned)o) t += y;
+    }
+    warp_tot[lane] = t;  // inclusive prefix over warps
+  }
+  __syncthreads();
+  uint32_t base = warp ? warp_tot[warp - 1] : 0u;
+  *total = warp_tot[nwarps - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// Decoupled look-back over tiles for a single running count.  Called by ONE
+// thread of the tile; `state` has one word per tile (zeroed before the
+// launch).  Returns the exclusive prefix of all earlier tiles.
+__device__ __forceinline__ uint32_t lookback_one(uint32_t* state, uint32_t tile,
+                                                 uint32_t agg) {
+  if (tile == 0) {
+    st_release(state, LB_INC | agg);
+    return 0u;
+  }
+  st_release(state + tile, LB_AGG | agg);
+  uint32_t excl = 0;
+  int t = (int)tile - 1;
+  while (true) {
+    uint32_t s = ld_acquire(state + t);
+    if ((s & ~LB_MASK) == 0u) continue;  // predecessor not published yet
+    excl += s & LB_MASK;
+    if (s & LB_INC) break;
+    --t;
+  }
+  st_release(state + tile, LB_INC | (excl + agg));
+  return excl;
+}
+
+}  // namespace lms

@@ -1,0 +1,686 @@
+// lmscale.cu -- host side of the C ABI declared in include/lmscale.h:
+// context, workspace, stream/event choreography of S1-S6 and NCCL.
+//
+// Step choreography of lmscale_sync_embedding_grad (one rank):
+//
+//   caller stream s  : [zero S3] -> ncclAllGather(J -> I) -> gbits(I) -> gscan -> l2g* -> scatter -> fixup -> ncclAllReduce(M)
+//   side stream      :  S1: [zero S1] -> radix hist -> radix passes -> segments --------^ (*waits)
+//   copy stream      :                                     D2H {U_g, err} after gscan
+//
+// The host blocks only on the 16-byte {U_g, err} copy, which lands while the
+// scatter kernel (already enqueued) runs; then it enqueues the all-reduce
+// with count U_g * D.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/lmscale.h"
+#include "kernels.cuh"
+
+using namespace lms;
+
+namespace {
+
+enum Ev {
+  EV_FORK = 0,
+  EV_S1_BEGIN,
+  EV_S1_END,
+  EV_GATHER_END,
+  EV_S3_END,
+  EV_JOIN,
+  EV_L2G_END,
+  EV_SCATTER_END,
+  EV_FIXUP_END,
+  EV_AR_END,
+  EV_UPD_BEGIN,
+  EV_UPD_END,
+  EV_COUNT
+};
+
+}  // namespace
+
+struct lmscale_ctx {
+  lmscale_config cfg;
+  int num_sms = 0;
+  int64_t K = 0, W = 0, NI = 0, ucap = 0, nchunks = 0, rtiles = 0, gtiles = 0;
+  SortPlan plan{};
+  cudaStream_t s_side = nullptr, s_copy = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_s1 = nullptr, ev_s3 = nullptr, ev_copy = nullptr;
+  cudaEvent_t tev[EV_COUNT] = {};
+  bool timing_valid = false, update_timed = false;
+  ncclComm_t comm = nullptr;
+  // device workspace
+  void* base = nullptr;
+  size_t ws_bytes = 0;
+  uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *hist, *lb_radix,
+      *lb_seg, *lb_gscan;
+  int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
+  float *M, *partial;
+  Sc1* sc1;
+  Sc3* sc3;
+  size_t r1_off = 0, r1_bytes = 0, r3_off = 0, r3_bytes = 0;
+  // lazily allocated
+  float* grad_all = nullptr;
+  uint32_t* stage_ids = nullptr;
+  float* stage_grad = nullptr;
+  // pinned host mirror of {Sc3, Sc1}
+  Sc3* h_sc3 = nullptr;
+  Sc1* h_sc1 = nullptr;
+  // call state
+  int64_t last_k = -1, last_n = -1;
+  bool have_s1 = false, have_s3 = false;
+  const uint32_t* sorted_keys = nullptr;
+  const int32_t* sorted_vals = nullptr;
+  int64_t last_ug = 0;
+  lmscale_stats stats{};
+  int kernels_call = 0;
+  int64_t kernels_total = 0;
+  char err[512] = {0};
+};
+
+namespace {
+
+lmscale_status fail(lmscale_ctx* c, lmscale_status st, const char* fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof(c->err), fmt, ap);
+    va_end(ap);
+  }
+  return st;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, LMSCALE_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,      \
+                  cudaGetErrorString(e_));                                               \
+  } while (0)
+
+#define NK(call)                                                                         \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(ctx, LMSCALE_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,      \
+                  ncclGetErrorString(r_));                                               \
+  } while (0)
+
+#define LAUNCHED(n)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, LMSCALE_ERR_CUDA, "%s:%d launch: %s", __FILE__, __LINE__,         \
+                  cudaGetErrorString(e_));                                               \
+    ctx->kernels_call += (n);                                                            \
+  } while (0)
+
+inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+bool comm_enabled(const lmscale_ctx* c) {
+  return c->cfg.world > 1 && !(c->cfg.flags & LMSCALE_FLAG_NO_COMM);
+}
+bool timing(const lmscale_ctx* c) { return (c->cfg.flags & LMSCALE_FLAG_TIMING) != 0; }
+
+void rec(lmscale_ctx* c, int ev, cudaStream_t s) {
+  if (timing(c)) cudaEventRecord(c->tev[ev], s);
+}
+
+void begin_call(lmscale_ctx* c) {
+  c->kernels_call = 0;
+  c->err[0] = 0;
+}
+void end_call(lmscale_ctx* c) {
+  c->kernels_total += c->kernels_call;
+  c->stats.kernels_last_call = c->kernels_call;
+  c->stats.kernels_total_lo = (int32_t)(c->kernels_total & 0x7fffffff);
+}
+
+// S1 on stream s: zero S1 state, histogram, LSD passes, run flags.
+lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t* nu_out,
+                      cudaStream_t s) {
+  const int K = (int)k;
+  CK(cudaMemsetAsync((char*)ctx->base + ctx->r1_off, 0, ctx->r1_bytes, s));
+  launch_radix_hist(ids, K, ctx->plan, ctx->hist, ctx->sc1, (uint32_t)ctx->cfg.vocab, s);
+  LAUNCHED(1);
+  const uint32_t* kin = ids;
+  const int32_t* vin = nullptr;
+  uint32_t* kb[2] = {ctx->keys_a, ctx->keys_b};
+  int32_t* vb[2] = {ctx->vals_a, ctx->vals_b};
+  for (int p = 0; p < ctx->plan.passes; ++p) {
+    launch_radix_pass(p, kin, vin, kb[p & 1], vb[p & 1], K, ctx->plan, ctx->hist,
+                      ctx->lb_radix, ctx->sc1, s);
+    LAUNCHED(1);
+    kin = kb[p & 1];
+    vin = vb[p & 1];
+  }
+  ctx->sorted_keys = kin;
+  ctx->sorted_vals = vin;
+  launch_segments(kin, vin, K, (uint32_t)ctx->cfg.vocab, ctx->luniq, ctx->lstart, ctx->segidx,
+                  ctx->inverse, ctx->lbits, ctx->sc1, ctx->lb_seg, nu_out, s);
+  LAUNCHED(1);
+  ctx->last_k = k;
+  ctx->have_s1 = true;
+  ctx->have_s3 = false;
+  return LMSCALE_OK;
+}
+
+// S3 bitmap + scan on stream s (the l2g map is launched separately: it
+// needs S1's J^).
+lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream_t s) {
+  CK(cudaMemsetAsync((char*)ctx->base + ctx->r3_off, 0, ctx->r3_bytes, s));
+  launch_gbits(I, n, (uint32_t)ctx->cfg.vocab, ctx->gbits, ctx->sc3, s);
+  LAUNCHED(1);
+  launch_gscan(ctx->gbits, ctx->W, ctx->wrank, ctx->ihat, ctx->sc3, ctx->lb_gscan, s);
+  LAUNCHED(1);
+  ctx->last_n = n;
+  return LMSCALE_OK;
+}
+
+lmscale_status run_l2g(lmscale_ctx* ctx, cudaStream_t s) {
+  launch_l2g(ctx->luniq, ctx->sc1, (int)ctx->last_k, (uint32_t)ctx->cfg.vocab, ctx->gbits,
+             ctx->wrank, ctx->l2g, s);
+  LAUNCHED(1);
+  ctx->have_s3 = true;
+  return LMSCALE_OK;
+}
+
+ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
+  ScatterArgs a;
+  a.grad = grad;
+  a.perm = ctx->sorted_vals;
+  a.segidx = ctx->segidx;
+  a.l2g = ctx->l2g;
+  a.lstart = ctx->lstart;
+  a.ihat = ctx->ihat;
+  a.lbits = ctx->lbits;
+  a.sc3 = ctx->sc3;
+  a.sc1 = ctx->sc1;
+  a.M = ctx->M;
+  a.partial = ctx->partial;
+  a.K = (int)ctx->last_k;
+  a.D = (int)ctx->cfg.dim;
+  a.ug_cap = std::min<int64_t>(ctx->last_n, ctx->cfg.vocab);
+  a.num_sms = ctx->num_sms;
+  return a;
+}
+
+lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s) {
+  ScatterArgs a = scatter_args(ctx, grad);
+  launch_scatter(a, s);
+  LAUNCHED(1);
+  rec(ctx, EV_SCATTER_END, s);
+  launch_fixup(a, s);
+  LAUNCHED(1);
+  return LMSCALE_OK;
+}
+
+lmscale_status check_ids_args(lmscale_ctx* ctx, const void* ids, int64_t k) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!ids) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "ids is NULL");
+  if (k < 1 || k > ctx->K)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "k=%lld outside [1, max_tokens=%lld]",
+                (long long)k, (long long)ctx->K);
+  return LMSCALE_OK;
+}
+
+float ev_ms(const lmscale_ctx* c, int a, int b) {
+  float ms = -1.f;
+  if (cudaEventElapsedTime(&ms, c->tev[a], c->tev[b]) != cudaSuccess) return -1.f;
+  return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lmscale_version(void) { return "lmscale 0.1 sm_100a"; }
+
+const char* lmscale_status_string(lmscale_status s) {
+  switch (s) {
+    case LMSCALE_OK: return "ok";
+    case LMSCALE_ERR_INVALID_ARG: return "invalid argument";
+    case LMSCALE_ERR_ID_RANGE: return "token id >= vocab";
+    case LMSCALE_ERR_CUDA: return "CUDA error";
+    case LMSCALE_ERR_NCCL: return "NCCL error";
+    case LMSCALE_ERR_OOM: return "out of device memory";
+    case LMSCALE_ERR_UNSUPPORTED: return "unsupported on this context";
+  }
+  return "unknown status";
+}
+
+const char* lmscale_last_error(const lmscale_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+lmscale_status lmscale_get_nccl_id(uint8_t out_id[128]) {
+  if (!out_id) return LMSCALE_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return LMSCALE_ERR_NCCL;
+  static_assert(sizeof(id) == 128, "NCCL unique id is 128 bytes");
+  memcpy(out_id, &id, 128);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
+                            lmscale_ctx** out) {
+  if (!out) return LMSCALE_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!cfg || cfg->vocab < 1 || cfg->vocab > 0xffffffffll || cfg->max_tokens < 1 ||
+      cfg->dim < 1 || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world ||
+      cfg->max_tokens > (1ll << 29) || (int64_t)cfg->world * cfg->max_tokens > (1ll << 30) ||
+      cfg->dim > (1ll << 20))
+    return LMSCALE_ERR_INVALID_ARG;
+  lmscale_ctx* ctx = new (std::nothrow) lmscale_ctx();
+  if (!ctx) return LMSCALE_ERR_OOM;
+  ctx->cfg = *cfg;
+  lmscale_status st = [&]() -> lmscale_status {
+    CK(cudaSetDevice(cfg->device));
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+    ctx->K = cfg->max_tokens;
+    ctx->W = (cfg->vocab + 31) / 32;
+    ctx->NI = (int64_t)cfg->world * cfg->max_tokens;
+    ctx->ucap = std::min<int64_t>(ctx->NI, cfg->vocab);
+    ctx->nchunks = (ctx->K + SC_CHUNK - 1) / SC_CHUNK;
+    ctx->rtiles = (ctx->K + RS_TILE - 1) / RS_TILE;
+    ctx->gtiles = (ctx->W + GS_TILE_WORDS - 1) / GS_TILE_WORDS;
+    ctx->plan = make_sort_plan((uint64_t)cfg->vocab);
+    const int64_t K = ctx->K, D = cfg->dim;
+    // ---- workspace layout (one allocation, 256-byte aligned sub-buffers)
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = off;
+      off = align_up(off + bytes);
+      return o;
+    };
+    size_t o_keys_a = take(4 * K), o_keys_b = take(4 * K), o_vals_a = take(4 * K),
+           o_vals_b = take(4 * K), o_segidx = take(4 * K), o_inverse = take(4 * K),
+           o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)), o_counts = take(4 * K),
+           o_l2g = take(4 * K), o_wrank = take(4 * ctx->W), o_I = take(4 * ctx->NI),
+           o_ihat = take(4 * ctx->ucap);
+    // zero region R1: Sc1 | hist | radix look-back | segment look-back | lbits
+    ctx->r1_off = off;
+    size_t o_sc1 = take(sizeof(Sc1)), o_hist = take(4 * RS_MAX_PASSES * 256),
+           o_lbr = take(4 * (size_t)RS_MAX_PASSES * ctx->rtiles * 256),
+           o_lbs = take(4 * ctx->rtiles), o_lbits = take(4 * ctx->W);
+    ctx->r1_bytes = off - ctx->r1_off;
+    // zero region R3: Sc3 | gscan look-back | gbits
+    ctx->r3_off = off;
+    size_t o_sc3 = take(sizeof(Sc3)), o_lbg = take(4 * ctx->gtiles), o_gbits = take(4 * ctx->W);
+    ctx->r3_bytes = off - ctx->r3_off;
+    size_t o_M = take(4 * (size_t)ctx->ucap * D);
+    size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
+    ctx->ws_bytes = off;
+    if (cudaMalloc(&ctx->base, off) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(%zu) failed", off);
+    }
+    char* b = (char*)ctx->base;
+    ctx->keys_a = (uint32_t*)(b + o_keys_a);
+    ctx->keys_b = (uint32_t*)(b + o_keys_b);
+    ctx->vals_a = (int32_t*)(b + o_vals_a);
+    ctx->vals_b = (int32_t*)(b + o_vals_b);
+    ctx->segidx = (int32_t*)(b + o_segidx);
+    ctx->inverse = (int32_t*)(b + o_inverse);
+    ctx->luniq = (uint32_t*)(b + o_luniq);
+    ctx->lstart = (int32_t*)(b + o_lstart);
+    ctx->counts = (int32_t*)(b + o_counts);
+    ctx->l2g = (int32_t*)(b + o_l2g);
+    ctx->wrank = (uint32_t*)(b + o_wrank);
+    ctx->I = (uint32_t*)(b + o_I);
+    ctx->ihat = (uint32_t*)(b + o_ihat);
+    ctx->sc1 = (Sc1*)(b + o_sc1);
+    ctx->hist = (uint32_t*)(b + o_hist);
+    ctx->lb_radix = (uint32_t*)(b + o_lbr);
+    ctx->lb_seg = (uint32_t*)(b + o_lbs);
+    ctx->lbits = (uint32_t*)(b + o_lbits);
+    ctx->sc3 = (Sc3*)(b + o_sc3);
+    ctx->lb_gscan = (uint32_t*)(b + o_lbg);
+    ctx->gbits = (uint32_t*)(b + o_gbits);
+    ctx->M = (float*)(b + o_M);
+    ctx->partial = (float*)(b + o_part);
+    CK(cudaMemset(ctx->base, 0, off));
+    CK(cudaHostAlloc((void**)&ctx->h_sc3, sizeof(Sc3) + sizeof(Sc1), cudaHostAllocDefault));
+    ctx->h_sc1 = (Sc1*)((char*)ctx->h_sc3 + sizeof(Sc3));
+    CK(cudaStreamCreateWithFlags(&ctx->s_side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_s3, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
+    if (timing(ctx))
+      for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&ctx->tev[i]));
+    if (comm_enabled(ctx)) {
+      if (!nccl_id) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "world > 1 needs an NCCL id");
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof(id));
+      NK(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
+    }
+    ctx->stats.workspace_bytes = (int64_t)off;
+    ctx->stats.us_dedup = ctx->stats.us_gather = ctx->stats.us_merge = ctx->stats.us_scatter =
+        ctx->stats.us_allreduce = ctx->stats.us_update = ctx->stats.us_total = -1.0;
+    return LMSCALE_OK;
+  }();
+  if (st != LMSCALE_OK) {
+    fprintf(stderr, "lmscale_init: %s\n", ctx->err);
+    lmscale_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return LMSCALE_OK;
+}
+
+void lmscale_destroy(lmscale_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (int i = 0; i < EV_COUNT; ++i)
+    if (ctx->tev[i]) cudaEventDestroy(ctx->tev[i]);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
+  if (ctx->ev_s3) cudaEventDestroy(ctx->ev_s3);
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  if (ctx->s_side) cudaStreamDestroy(ctx->s_side);
+  if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
+  if (ctx->h_sc3) cudaFreeHost(ctx->h_sc3);
+  if (ctx->base) cudaFree(ctx->base);
+  if (ctx->grad_all) cudaFree(ctx->grad_all);
+  if (ctx->stage_ids) cudaFree(ctx->stage_ids);
+  if (ctx->stage_grad) cudaFree(ctx->stage_grad);
+  delete ctx;
+}
+
+// ------------------------------------------------------------- staged calls
+
+lmscale_status lmscale_unique(lmscale_ctx* ctx, const uint32_t* ids, int64_t k,
+                              uint32_t* uniq_out, int32_t* counts_out, int32_t* inverse_out,
+                              int64_t* num_unique_out, void* stream) {
+  lmscale_status st = check_ids_args(ctx, ids, k);
+  if (st) return st;
+  begin_call(ctx);
+  cudaStream_t s = S(stream);
+  st = run_s1(ctx, ids, k, num_unique_out, s);
+  if (st) return st;
+  if (uniq_out || counts_out || inverse_out) {
+    launch_counts_export(ctx->lstart, ctx->luniq, ctx->inverse, ctx->sc1, (int)k, ctx->counts,
+                         uniq_out, counts_out, inverse_out, s);
+    LAUNCHED(1);
+  }
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_global_unique(lmscale_ctx* ctx, const uint32_t* gathered, int64_t n,
+                                     void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!gathered || n < 1 || n > ctx->NI)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "gathered/n invalid (n=%lld, cap %lld)",
+                (long long)n, (long long)ctx->NI);
+  if (!ctx->have_s1) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "call lmscale_unique first");
+  begin_call(ctx);
+  cudaStream_t s = S(stream);
+  lmscale_status st = run_s3(ctx, gathered, n, s);
+  if (st) return st;
+  st = run_l2g(ctx, s);
+  if (st) return st;
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_scatter_expand(lmscale_ctx* ctx, const float* grad, int64_t k,
+                                      void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!grad) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad is NULL");
+  if (!ctx->have_s3 || k != ctx->last_k)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG,
+                "call lmscale_unique and lmscale_global_unique first (same k)");
+  begin_call(ctx);
+  lmscale_status st = run_s4(ctx, grad, S(stream));
+  if (st) return st;
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_get_sparse_grad(lmscale_ctx* ctx, lmscale_sparse_grad* out,
+                                       void* stream) {
+  if (!ctx || !out) return LMSCALE_ERR_INVALID_ARG;
+  if (!ctx->have_s3) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "no exchange computed yet");
+  CK(cudaStreamSynchronize(S(stream)));
+  CK(cudaMemcpy(ctx->h_sc3, ctx->sc3, sizeof(Sc3), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ctx->h_sc1, ctx->sc1, sizeof(Sc1), cudaMemcpyDeviceToHost));
+  out->ids = ctx->ihat;
+  out->rows = ctx->M;
+  out->num_unique = ctx->h_sc3->u_global;
+  ctx->stats.u_global = ctx->h_sc3->u_global;
+  ctx->stats.u_local = ctx->h_sc1->u_local;
+  if ((ctx->h_sc3->err | ctx->h_sc1->err) & 1u)
+    return fail(ctx, LMSCALE_ERR_ID_RANGE, "a token id >= vocab (%lld)",
+                (long long)ctx->cfg.vocab);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_get_local_maps(lmscale_ctx* ctx, const uint32_t** uniq,
+                                      const int32_t** counts, const int32_t** inverse,
+                                      const int32_t** l2g, int64_t* num_unique_local,
+                                      void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!ctx->have_s1) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "no S1 computed yet");
+  cudaStream_t s = S(stream);
+  launch_counts_export(ctx->lstart, ctx->luniq, ctx->inverse, ctx->sc1, (int)ctx->last_k,
+                       ctx->counts, nullptr, nullptr, nullptr, s);
+  LAUNCHED(1);
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpy(ctx->h_sc1, ctx->sc1, sizeof(Sc1), cudaMemcpyDeviceToHost));
+  if (uniq) *uniq = ctx->luniq;
+  if (counts) *counts = ctx->counts;
+  if (inverse) *inverse = ctx->inverse;
+  if (l2g) *l2g = ctx->have_s3 ? ctx->l2g : nullptr;
+  if (num_unique_local) *num_unique_local = ctx->h_sc1->u_local;
+  return LMSCALE_OK;
+}
+
+// ----------------------------------------------------------- collective path
+
+lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids,
+                                           const float* grad, int64_t k,
+                                           lmscale_sparse_grad* out, void* stream) {
+  lmscale_status st = check_ids_args(ctx, ids, k);
+  if (st) return st;
+  if (!grad || !out) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad/out is NULL");
+  if ((ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
+    return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "collective call on a NO_COMM context");
+  begin_call(ctx);
+  cudaStream_t s = S(stream);
+  const int G = ctx->cfg.world;
+  const int64_t D = ctx->cfg.dim;
+  ctx->timing_valid = false;
+  ctx->update_timed = false;
+  rec(ctx, EV_FORK, s);
+  // S1 on the side stream, concurrent with the ID all-gather.
+  CK(cudaEventRecord(ctx->ev_fork, s));
+  CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_fork, 0));
+  rec(ctx, EV_S1_BEGIN, ctx->s_side);
+  st = run_s1(ctx, ids, k, nullptr, ctx->s_side);
+  if (st) return st;
+  rec(ctx, EV_S1_END, ctx->s_side);
+  CK(cudaEventRecord(ctx->ev_s1, ctx->s_side));
+  // S2: all-gather of J.
+  const uint32_t* I = ids;
+  int64_t n = k;
+  if (G > 1) {
+    NK(ncclAllGather(ids, ctx->I, (size_t)k, ncclUint32, ctx->comm, s));
+    I = ctx->I;
+    n = (int64_t)G * k;
+  }
+  rec(ctx, EV_GATHER_END, s);
+  // S3: I^, U_g; U_g + error flag to the host on the copy stream.
+  st = run_s3(ctx, I, n, s);
+  if (st) return st;
+  rec(ctx, EV_S3_END, s);
+  CK(cudaEventRecord(ctx->ev_s3, s));
+  CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_s3, 0));
+  CK(cudaMemcpyAsync(ctx->h_sc3, ctx->sc3, sizeof(Sc3), cudaMemcpyDeviceToHost, ctx->s_copy));
+  CK(cudaEventRecord(ctx->ev_copy, ctx->s_copy));
+  // join S1, then l2g + S4.
+  CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
+  rec(ctx, EV_JOIN, s);
+  st = run_l2g(ctx, s);
+  if (st) return st;
+  rec(ctx, EV_L2G_END, s);
+  st = run_s4(ctx, grad, s);
+  if (st) return st;
+  rec(ctx, EV_FIXUP_END, s);
+  // host learns U_g (hidden behind the scatter kernel)
+  CK(cudaEventSynchronize(ctx->ev_copy));
+  const int64_t ug = ctx->h_sc3->u_global;
+  ctx->last_ug = ug;
+  ctx->stats.u_global = ug;
+  if (ctx->h_sc3->err & 1u) {
+    end_call(ctx);
+    return fail(ctx, LMSCALE_ERR_ID_RANGE, "a token id >= vocab (%lld)",
+                (long long)ctx->cfg.vocab);
+  }
+  // S5: all-reduce of M.
+  if (G > 1 && ug > 0) NK(ncclAllReduce(ctx->M, ctx->M, (size_t)(ug * D), ncclFloat, ncclSum,
+                                        ctx->comm, s));
+  rec(ctx, EV_AR_END, s);
+  out->ids = ctx->ihat;
+  out->rows = ctx->M;
+  out->num_unique = ug;
+  ctx->stats.bytes_ids_gathered = 4 * (int64_t)(G - 1) * k;
+  ctx->stats.bytes_grad_allreduce = G > 1 ? 4 * ug * D : 0;
+  ctx->stats.bytes_scatter = 4 * k * D + 4 * ug * D;
+  ctx->stats.bytes_update = 12 * ug * D;
+  ctx->timing_valid = timing(ctx);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_apply_sparse_update(lmscale_ctx* ctx, float* table,
+                                           const lmscale_sparse_grad* sg, float lr,
+                                           void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!table || !sg || (sg->num_unique > 0 && (!sg->ids || !sg->rows)) || sg->num_unique < 0 ||
+      sg->num_unique > ctx->cfg.vocab)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "table/sg invalid");
+  begin_call(ctx);
+  cudaStream_t s = S(stream);
+  rec(ctx, EV_UPD_BEGIN, s);
+  launch_update(table, (int)ctx->cfg.dim, sg->ids, sg->rows, sg->num_unique, lr, ctx->num_sms, s);
+  if (sg->num_unique > 0) LAUNCHED(1);
+  rec(ctx, EV_UPD_END, s);
+  ctx->update_timed = timing(ctx);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_dense_apply(lmscale_ctx* ctx, const uint32_t* ids, const float* grad,
+                                   int64_t n, float* table, float lr, void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!ids || !grad || !table || n < 1 || n > ctx->NI)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "dense_apply args invalid");
+  begin_call(ctx);
+  launch_dense(table, (int)ctx->cfg.dim, ids, grad, n, lr, (uint32_t)ctx->cfg.vocab,
+               ctx->num_sms, S(stream));
+  LAUNCHED(1);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_sync_dense_baseline(lmscale_ctx* ctx, const uint32_t* ids,
+                                           const float* grad, int64_t k, float* table,
+                                           float lr, void* stream) {
+  lmscale_status st = check_ids_args(ctx, ids, k);
+  if (st) return st;
+  if (!grad || !table) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad/table is NULL");
+  if ((ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
+    return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "collective call on a NO_COMM context");
+  begin_call(ctx);
+  cudaStream_t s = S(stream);
+  const int G = ctx->cfg.world;
+  const int64_t D = ctx->cfg.dim;
+  const uint32_t* I = ids;
+  const float* A = grad;
+  if (G > 1) {
+    if (!ctx->grad_all) {
+      if (cudaMalloc(&ctx->grad_all, 4 * (size_t)ctx->NI * D) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->grad_all = nullptr;
+        return fail(ctx, LMSCALE_ERR_OOM, "dense gather buffer (%lld bytes)",
+                    (long long)(4 * ctx->NI * D));
+      }
+    }
+    NK(ncclGroupStart());
+    NK(ncclAllGather(ids, ctx->I, (size_t)k, ncclUint32, ctx->comm, s));
+    NK(ncclAllGather(grad, ctx->grad_all, (size_t)(k * D), ncclFloat, ctx->comm, s));
+    NK(ncclGroupEnd());
+    I = ctx->I;
+    A = ctx->grad_all;
+  }
+  launch_dense(table, (int)D, I, A, (int64_t)G * k, lr, (uint32_t)ctx->cfg.vocab, ctx->num_sms,
+               s);
+  LAUNCHED(1);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_train_step_host(lmscale_ctx* ctx, const uint32_t* ids_host,
+                                       const float* grad_host, int64_t k, float* table, float lr,
+                                       uint32_t* ids_out_host, int64_t* num_unique_out,
+                                       void* stream) {
+  lmscale_status st = check_ids_args(ctx, ids_host, k);
+  if (st) return st;
+  if (!grad_host || !table) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad/table is NULL");
+  const int64_t D = ctx->cfg.dim;
+  if (!ctx->stage_ids) {
+    if (cudaMalloc(&ctx->stage_ids, 4 * (size_t)ctx->K) != cudaSuccess ||
+        cudaMalloc(&ctx->stage_grad, 4 * (size_t)ctx->K * D) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, LMSCALE_ERR_OOM, "host-step staging buffers");
+    }
+  }
+  cudaStream_t s = S(stream);
+  CK(cudaMemcpyAsync(ctx->stage_ids, ids_host, 4 * (size_t)k, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->stage_grad, grad_host, 4 * (size_t)k * D, cudaMemcpyHostToDevice, s));
+  lmscale_sparse_grad sg;
+  st = lmscale_sync_embedding_grad(ctx, ctx->stage_ids, ctx->stage_grad, k, &sg, stream);
+  if (st) return st;
+  int kc = ctx->kernels_call;
+  st = lmscale_apply_sparse_update(ctx, table, &sg, lr, stream);
+  if (st) return st;
+  ctx->kernels_call += kc;
+  ctx->stats.kernels_last_call = ctx->kernels_call;
+  if (ids_out_host && sg.num_unique > 0)
+    CK(cudaMemcpyAsync(ids_out_host, sg.ids, 4 * (size_t)sg.num_unique, cudaMemcpyDeviceToHost,
+                       s));
+  if (num_unique_out) *num_unique_out = sg.num_unique;
+  CK(cudaStreamSynchronize(s));
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
+  if (!cctx || !out) return LMSCALE_ERR_INVALID_ARG;
+  lmscale_ctx* ctx = const_cast<lmscale_ctx*>(cctx);
+  lmscale_stats& st = ctx->stats;
+  if (ctx->timing_valid) {
+    CK(cudaEventSynchronize(ctx->tev[EV_AR_END]));
+    if (ctx->update_timed) CK(cudaEventSynchronize(ctx->tev[EV_UPD_END]));
+    st.us_dedup = 1e3 * ev_ms(ctx, EV_S1_BEGIN, EV_S1_END);
+    st.us_gather = 1e3 * ev_ms(ctx, EV_FORK, EV_GATHER_END);
+    st.us_merge = 1e3 * ev_ms(ctx, EV_GATHER_END, EV_S3_END);
+    st.us_scatter = 1e3 * ev_ms(ctx, EV_L2G_END, EV_SCATTER_END);
+    st.us_allreduce = 1e3 * ev_ms(ctx, EV_FIXUP_END, EV_AR_END);
+    st.us_update = ctx->update_timed ? 1e3 * ev_ms(ctx, EV_UPD_BEGIN, EV_UPD_END) : -1.0;
+    st.us_total = 1e3 * ev_ms(ctx, EV_FORK, ctx->update_timed ? EV_UPD_END : EV_AR_END);
+  }
+  *out = st;
+  return LMSCALE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,400 @@
+// scatter.cu -- S4 segmented scatter-add (steps 2+5),
+// S6 duplicate-free row update (step 7) and the S0 dense
+// comparison scatter for sm_100a.
+//
+// S4 layout: the K gradient rows are visited in sorted-id order through the
+// stable permutation from S1.  Work items are (chunk of 32 sorted positions,
+// column block) pairs, one warp each, in a persistent grid: every warp reads
+// its 32 rows with 128-bit streaming loads (4-row software pipeline), sums the
+// runs of equal ids in registers and writes each finished run ONCE to its
+// global slot of M.  Runs cut by a chunk boundary write a partial row instead
+// (head / tail partial of the chunk); a second launch sums each cut run's
+// partials in a fixed order (deterministic, no atomics) and writes its M row.
+// Slots whose word is absent on this rank are written as zeros by extra work
+// items, so every one of the U_g rows is stored exactly once (no memset).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace lms {
+
+namespace {
+
+// Vector traits: float4 (128-bit path, dim % 4 == 0) or float (any dim).
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float4> {
+  static constexpr int W = 4;
+  __device__ __forceinline__ static float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ static float4 ld_once(const float4* p) { return ld_stream(p); }
+  __device__ __forceinline__ static float4 ld_l2(const float4* p) { return ld_cg(p); }
+  __device__ __forceinline__ static void st(float4* p, float4 v) { st_v4(p, v); }
+  __device__ __forceinline__ static float4 add(float4 a, float4 b) { return f4add(a, b); }
+  __device__ __forceinline__ static float4 fma(float s, float4 a, float4 b) {
+    return make_float4(__fmaf_rn(s, a.x, b.x), __fmaf_rn(s, a.y, b.y), __fmaf_rn(s, a.z, b.z),
+                       __fmaf_rn(s, a.w, b.w));
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int W = 1;
+  __device__ __forceinline__ static float zero() { return 0.f; }
+  __device__ __forceinline__ static float ld_once(const float* p) { return __ldcs(p); }
+  __device__ __forceinline__ static float ld_l2(const float* p) { return __ldcg(p); }
+  __device__ __forceinline__ static void st(float* p, float v) { *p = v; }
+  __device__ __forceinline__ static float add(float a, float b) { return a + b; }
+  __device__ __forceinline__ static float fma(float s, float a, float b) {
+    return __fmaf_rn(s, a, b);
+  }
+};
+
+constexpr int SC_THREADS = 256;
+constexpr int FX_THREADS = 512;
+
+}  // namespace
+
+// ------------------------------------------------------------------- S4
+
+template <typename T, int NV, int UNR>
+__global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
+  using V = Vec<T>;
+  const int K = a.K;
+  const int C = a.D / V::W;  // vectors per row
+  const int ncb = (C + 32 * NV - 1) / (32 * NV);
+  const int nchunks = (K + SC_CHUNK - 1) / SC_CHUNK;
+  const int64_t Ug = a.sc3->u_global;
+  const int64_t nz = (Ug + SC_ZGROUP - 1) / SC_ZGROUP;
+  const int64_t items = ((int64_t)nchunks + nz) * ncb;
+  const int lane = (int)lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* g = reinterpret_cast<const T*>(a.grad);
+  T* M = reinterpret_cast<T*>(a.M);
+  T* P = reinterpret_cast<T*>(a.partial);
+
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
+       it += nwarps) {
+    const int cb = (int)(it % ncb);
+    const int64_t unit = it / ncb;
+    const int col0 = cb * 32 * NV + lane;
+    if (unit < nchunks) {
+      // ---- chunk of sorted positions [i0, i0 + n)
+      const int c = (int)unit;
+      const int i0 = c * SC_CHUNK;
+      const int n = min(SC_CHUNK, K - i0);
+      int my_pos = 0, my_u = -1, my_slot = -1;
+      if (lane < n) {
+        my_pos = __ldg(a.perm + i0 + lane);
+        my_u = __ldg(a.segidx + i0 + lane);
+        my_slot = __ldg(a.l2g + my_u);
+      }
+      const int prev_u = i0 > 0 ? __ldg(a.segidx + i0 - 1) : -1;
+      const int next_u = i0 + n < K ? __ldg(a.segidx + i0 + n) : -1;
+      const int up = __shfl_up_sync(FULL, my_u, 1);
+      const unsigned hmask = __ballot_sync(FULL, lane < n && (lane == 0 || my_u != up));
+      const bool split_left = __shfl_sync(FULL, my_u, 0) == prev_u;
+      const bool split_right = __shfl_sync(FULL, my_u, n - 1) == next_u;
+      T acc[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+      int seg_first = 1;  // the run being accumulated is the chunk's first
+      for (int p0 = 0; p0 < n; p0 += UNR) {
+        T r[UNR][NV];
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const int p = p0 + q;
+          const int pos = __shfl_sync(FULL, my_pos, p & 31);
+          const T* row = g + (size_t)pos * C;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int col = col0 + v * 32;
+            r[q][v] = (p < n && col < C) ? V::ld_once(row + col) : V::zero();
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const int p = p0 + q;
+          if (p < n) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
+            const bool last = (p == n - 1);
+            if (last || ((hmask >> (p + 1)) & 1u)) {
+              const int slot = __shfl_sync(FULL, my_slot, p);
+              T* dst;
+              if (seg_first && split_left)
+                dst = P + (size_t)(2 * c) * C;
+              else if (last && split_right)
+                dst = P + (size_t)(2 * c + 1) * C;
+              else
+                dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
+              if (dst) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                  const int col = col0 + v * 32;
+                  if (col < C) V::st(dst + col, acc[v]);
+                }
+              }
+#pragma unroll
+              for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+              seg_first = 0;
+            }
+          }
+        }
+      }
+    } else {
+      // ---- zero rows: slots [r0, r0 + 32) whose word is absent on this rank
+      const int64_t r0 = (unit - nchunks) * SC_ZGROUP;
+      const int64_t r = r0 + lane;
+      bool absent = false;
+      if (r < Ug) {
+        const uint32_t w = __ldg(a.ihat + r);
+        absent = !((__ldg(a.lbits + (w >> 5)) >> (w & 31u)) & 1u);
+      }
+      unsigned am = __ballot_sync(FULL, absent);
+      while (am) {
+        const int b = __ffs(am) - 1;
+        am &= am - 1;
+        T* dst = M + (size_t)(r0 + b) * C;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int col = col0 + v * 32;
+          if (col < C) V::st(dst + col, V::zero());
+        }
+      }
+    }
+  }
+}
+
+// Sum the partials of every run cut by a chunk boundary.  Work item =
+// (chunk c that holds the START of a run continuing into chunk c+1, column
+// block); the run's partials are P[2c+1] (tail of c) and P[2c'] (head) for
+// c < c' <= c1.  Warp w sums partials w, w+16, ... in order; warps are then
+// combined in warp order through shared memory (deterministic).
+template <typename T, int NV>
+__global__ void __launch_bounds__(FX_THREADS) k_fixup(ScatterArgs a) {
+  using V = Vec<T>;
+  constexpr int NWF = FX_THREADS / 32;
+  constexpr int UNR = 4;
+  __shared__ T red[NWF][32 * NV];
+  const int K = a.K;
+  const int C = a.D / V::W;
+  const int ncb = (C + 32 * NV - 1) / (32 * NV);
+  const int nchunks = (K + SC_CHUNK - 1) / SC_CHUNK;
+  const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
+  const T* P = reinterpret_cast<const T*>(a.partial);
+  T* M = reinterpret_cast<T*>(a.M);
+  const int64_t items = (int64_t)nchunks * ncb;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int c = (int)(it / ncb);
+    const int cb = (int)(it % ncb);
+    const int iend = min(K, (c + 1) * SC_CHUNK);
+    if (iend >= K) continue;
+    const int u = __ldg(a.segidx + iend - 1);
+    if (__ldg(a.segidx + iend) != u) continue;      // run ends inside chunk c
+    const int s0 = __ldg(a.lstart + u);
+    if (s0 < c * SC_CHUNK) continue;                 // run owned by an earlier chunk
+    const int c1 = (__ldg(a.lstart + u + 1) - 1) / SC_CHUNK;
+    const int np = c1 - c + 1;
+    const int slot = __ldg(a.l2g + u);
+    const int col0 = cb * 32 * NV + lane;
+    T acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+    for (int k0 = warp; k0 < np; k0 += NWF * UNR) {
+      T r[UNR][NV];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int k = k0 + q * NWF;
+        const size_t prow = k == 0 ? (size_t)(2 * c + 1) : (size_t)(2 * (c + k));
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int col = col0 + v * 32;
+          r[q][v] = (k < np && col < C) ? V::ld_l2(P + prow * C + col) : V::zero();
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) red[warp][v * 32 + lane] = acc[v];
+    __syncthreads();
+    if (warp == 0 && slot >= 0) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        T s = red[0][v * 32 + lane];
+        for (int w = 1; w < NWF; ++w) s = V::add(s, red[w][v * 32 + lane]);
+        const int col = col0 + v * 32;
+        if (col < C) V::st(M + (size_t)slot * C + col, s);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+namespace {
+template <typename T>
+bool vec_ok(const ScatterArgs& a) {
+  if (sizeof(T) == 4) return true;
+  return (a.D % 4 == 0) && ((uintptr_t)a.grad % 16 == 0) && ((uintptr_t)a.M % 16 == 0) &&
+         ((uintptr_t)a.partial % 16 == 0);
+}
+}  // namespace
+
+template <typename T, int NV, int UNR>
+static void scatter_t(const ScatterArgs& a, cudaStream_t s) {
+  const int C = a.D / Vec<T>::W;
+  const int ncb = (C + 32 * NV - 1) / (32 * NV);
+  const int64_t nchunks = (a.K + SC_CHUNK - 1) / SC_CHUNK;
+  const int64_t nz = (a.ug_cap + SC_ZGROUP - 1) / SC_ZGROUP;
+  const int64_t warps = (nchunks + nz) * ncb;
+  int64_t blocks = (warps * 32 + SC_THREADS - 1) / SC_THREADS;
+  static int occ = 0;  // resident CTAs per SM for this instantiation (persistent grid)
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<T, NV, UNR>, SC_THREADS,
+                                                      0) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  const int64_t cap = (int64_t)a.num_sms * occ;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_scatter<T, NV, UNR><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
+}
+
+template <typename T, int NV>
+static void fixup_t(const ScatterArgs& a, cudaStream_t s) {
+  const int C = a.D / Vec<T>::W;
+  const int ncb = (C + 32 * NV - 1) / (32 * NV);
+  const int64_t nchunks = (a.K + SC_CHUNK - 1) / SC_CHUNK;
+  int64_t blocks = nchunks * ncb;
+  const int64_t cap = (int64_t)a.num_sms * 4;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_fixup<T, NV><<<(unsigned)blocks, FX_THREADS, 0, s>>>(a);
+}
+
+void launch_scatter(const ScatterArgs& a, cudaStream_t s) {
+  if (vec_ok<float4>(a)) {
+    const int C = a.D / 4;
+    if (C >= 128)
+      scatter_t<float4, 4, 4>(a, s);
+    else if (C >= 64)
+      scatter_t<float4, 2, 4>(a, s);
+    else
+      scatter_t<float4, 1, 4>(a, s);
+  } else {
+    scatter_t<float, 4, 4>(a, s);
+  }
+}
+
+void launch_fixup(const ScatterArgs& a, cudaStream_t s) {
+  if (vec_ok<float4>(a)) {
+    const int C = a.D / 4;
+    if (C >= 128)
+      fixup_t<float4, 4>(a, s);
+    else if (C >= 64)
+      fixup_t<float4, 2>(a, s);
+    else
+      fixup_t<float4, 1>(a, s);
+  } else {
+    fixup_t<float, 4>(a, s);
+  }
+}
+
+// ------------------------------------------------------------------- S6
+// table[ids[r]] = fma(-lr, rows[r], table[ids[r]]) for r < n.  One warp per
+// row at a time (rows are disjoint: P:433-435), 128-bit accesses.
+template <typename T>
+__global__ void __launch_bounds__(256) k_update(float* __restrict__ table, int D,
+                                                const uint32_t* __restrict__ ids,
+                                                const float* __restrict__ rows, int64_t n,
+                                                float lr) {
+  using V = Vec<T>;
+  const int C = D / V::W;
+  const int lane = (int)lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* R = reinterpret_cast<const T*>(rows);
+  T* E = reinterpret_cast<T*>(table);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nwarps) {
+    const uint32_t w = __ldg(ids + r);
+    const T* src = R + (size_t)r * C;
+    T* dst = E + (size_t)w * C;
+    int col = lane;
+    for (; col + 96 < C; col += 128) {
+      T m0 = V::ld_once(src + col), m1 = V::ld_once(src + col + 32);
+      T m2 = V::ld_once(src + col + 64), m3 = V::ld_once(src + col + 96);
+      T e0 = dst[col], e1 = dst[col + 32], e2 = dst[col + 64], e3 = dst[col + 96];
+      V::st(dst + col, V::fma(-lr, m0, e0));
+      V::st(dst + col + 32, V::fma(-lr, m1, e1));
+      V::st(dst + col + 64, V::fma(-lr, m2, e2));
+      V::st(dst + col + 96, V::fma(-lr, m3, e3));
+    }
+    for (; col < C; col += 32) V::st(dst + col, V::fma(-lr, V::ld_once(src + col), dst[col]));
+  }
+}
+
+void launch_update(float* table, int D, const uint32_t* ids, const float* rows, int64_t n,
+                   float lr, int num_sms, cudaStream_t s) {
+  if (n <= 0) return;
+  int64_t blocks = (n + 7) / 8;
+  const int64_t cap = (int64_t)num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)rows % 16 == 0;
+  if (v4)
+    k_update<float4><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, lr);
+  else
+    k_update<float><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, lr);
+}
+
+// ------------------------------------------------------------------- S0
+// Dense comparison path: table[ids[q]] += -lr * grad[q] for every one of the
+// n gathered tokens, 128-bit vector reductions at L2 (red.global.add.v4.f32):
+// the GPU analogue of the paper's locked row updates.
+__global__ void __launch_bounds__(256) k_dense_v4(float* __restrict__ table, int D,
+                                                  const uint32_t* __restrict__ ids,
+                                                  const float* __restrict__ grad, int64_t n,
+                                                  float lr, uint32_t vocab) {
+  const int C = D / 4;
+  const int lane = (int)lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float4* G4 = reinterpret_cast<const float4*>(grad);
+  float4* E4 = reinterpret_cast<float4*>(table);
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n; q += nwarps) {
+    const uint32_t w = __ldg(ids + q);
+    if (w >= vocab) continue;
+    const float4* src = G4 + (size_t)q * C;
+    float4* dst = E4 + (size_t)w * C;
+    for (int col = lane; col < C; col += 32) {
+      float4 v = ld_stream(src + col);
+      red_add_v4(dst + col, make_float4(-lr * v.x, -lr * v.y, -lr * v.z, -lr * v.w));
+    }
+  }
+}
+__global__ void __launch_bounds__(256) k_dense_s(float* __restrict__ table, int D,
+                                                 const uint32_t* __restrict__ ids,
+                                                 const float* __restrict__ grad, int64_t n,
+                                                 float lr, uint32_t vocab) {
+  const int lane = (int)lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n; q += nwarps) {
+    const uint32_t w = __ldg(ids + q);
+    if (w >= vocab) continue;
+    for (int col = lane; col < D; col += 32)
+      atomicAdd(table + (size_t)w * D + col, -lr * __ldcs(grad + (size_t)q * D + col));
+  }
+}
+
+void launch_dense(float* table, int D, const uint32_t* ids, const float* grad, int64_t n,
+                  float lr, uint32_t vocab, int num_sms, cudaStream_t s) {
+  if (n <= 0) return;
+  int64_t blocks = (n + 7) / 8;
+  const int64_t cap = (int64_t)num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)grad % 16 == 0;
+  if (v4)
+    k_dense_v4<<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, grad, n, lr, vocab);
+  else
+    k_dense_s<<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, grad, n, lr, vocab);
+}
+
+}  // namespace lms

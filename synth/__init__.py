@@ -123,7 +123,11 @@ def _key(seed: int, tag: int, rank: int, step: int) -> int:
 
 def counter_bits(n: int, key: int, device="cpu", offset: int = 0) -> torch.Tensor:
     """32-bit hash of element indices offset..offset+n-1 under ``key`` (int64)."""
-    idx = torch.arange(offset, offset + n, dtype=torch.int64, device=device)
+    return hash_index(torch.arange(offset, offset + n, dtype=torch.int64, device=device), key)
+
+
+def hash_index(idx: torch.Tensor, key: int) -> torch.Tensor:
+    """32-bit hash of int64 element indices under ``key``."""
     lo = idx & 0xFFFFFFFF
     hi = idx >> 32
     x = _mix32(lo ^ key)
@@ -144,14 +148,42 @@ def _to_value(bits: torch.Tensor, kind: str) -> torch.Tensor:
     raise ValueError(kind)
 
 
+def _fill(out: torch.Tensor, key: int, kind: str, row0: int) -> torch.Tensor:
+    rows, D = out.shape
+    chunk = max(1, (1 << 26) // max(D, 1))          # bound the int64 temporaries
+    for r in range(0, rows, chunk):
+        n = min(chunk, rows - r)
+        bits = counter_bits(n * D, key, out.device, offset=(row0 + r) * D)
+        out[r:r + n] = _to_value(bits, kind).view(n, D)
+    return out
+
+
+def _rows(D: int, positions, key: int, kind: str) -> torch.Tensor:
+    pos = torch.as_tensor(np.asarray(positions, np.int64)).reshape(-1)
+    idx = (pos[:, None] * D + torch.arange(D, dtype=torch.int64)[None, :]).reshape(-1)
+    return _to_value(hash_index(idx, key), kind).view(len(pos), D)
+
+
+_GKIND = {"int": "int_grad", "pos": "pos", "signed": "signed"}
+
+
 def grad_values(K: int, D: int, mode: str, rank: int = 0, step: int = 0,
                 seed: int = MASTER_SEED, device="cpu", row0: int = 0,
                 rows: int | None = None) -> torch.Tensor:
     """Delta_g (K x D fp32) or rows row0..row0+rows-1 of it."""
     rows = K - row0 if rows is None else rows
-    bits = counter_bits(rows * D, _key(seed, _TAG_GRAD, rank, step), device, offset=row0 * D)
-    kind = {"int": "int_grad", "pos": "pos", "signed": "signed"}[mode]
-    return _to_value(bits, kind).view(rows, D)
+    out = torch.empty(rows, D, dtype=torch.float32, device=device)
+    return _fill(out, _key(seed, _TAG_GRAD, rank, step), _GKIND[mode], row0)
+
+
+def grad_rows(D: int, mode: str, positions, rank: int = 0, step: int = 0,
+              seed: int = MASTER_SEED) -> torch.Tensor:
+    """Rows ``positions`` of Delta_g (len(positions) x D) without drawing the rest."""
+    return _rows(D, positions, _key(seed, _TAG_GRAD, rank, step), _GKIND[mode])
+
+
+def _tkind(mode: str) -> str:
+    return "int_table" if mode == "int" else "signed"
 
 
 def table_values(V: int, D: int, mode: str, seed: int = MASTER_SEED, device="cpu",
@@ -159,22 +191,12 @@ def table_values(V: int, D: int, mode: str, seed: int = MASTER_SEED, device="cpu
     """E0 (V x D fp32) or rows row0..row0+rows-1 of it; identical on every rank."""
     rows = V - row0 if rows is None else rows
     out = torch.empty(rows, D, dtype=torch.float32, device=device)
-    kind = "int_table" if mode == "int" else "signed"
-    key = _key(seed, _TAG_TABLE, 0, 0)
-    chunk = max(1, (1 << 26) // max(D, 1))          # bound temporaries
-    for r in range(0, rows, chunk):
-        n = min(chunk, rows - r)
-        out[r:r + n] = _to_value(counter_bits(n * D, key, device, offset=(row0 + r) * D), kind).view(n, D)
-    return out
+    return _fill(out, _key(seed, _TAG_TABLE, 0, 0), _tkind(mode), row0)
 
 
 def table_rows(V: int, D: int, mode: str, ids, seed: int = MASTER_SEED) -> torch.Tensor:
     """E0[ids] on the CPU without materialising the V x D table."""
-    ids = np.asarray(ids, dtype=np.int64)
-    out = torch.empty(len(ids), D, dtype=torch.float32)
-    for i, w in enumerate(ids):
-        out[i] = table_values(V, D, mode, seed=seed, row0=int(w), rows=1)[0]
-    return out
+    return _rows(D, ids, _key(seed, _TAG_TABLE, 0, 0), _tkind(mode))
 
 
 def default_lr(mode: str) -> float:

@@ -1,0 +1,350 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, on the same
+seeded inputs (synth).  Integers (J^, counts, inverse, I^, U_g, l2g) must be
+bit-exact; floats meet tests/tolerances.py (INT mode bit-exact).
+
+* small configs: element-by-element over every output;
+* BASELINE.json full sizes (1b / char / amazon / tieba at G=1, the launch
+  configuration bench.py times): integers in full, float rows sampled (the
+  hottest words -- the longest segments, which exercise the chunk-split fixup
+  -- plus random words), each row computed by the oracle from its definition;
+* G > 1 emulated on one GPU with a NO_COMM context per the staged ABI
+  (torch.cat stands in for the all-gather, a rank-ordered fp32 sum for the
+  all-reduce -- labelled emulation, not a backend).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.tolerances import check_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lm():
+    from paper_1810_10045_b200 import lmscale
+    return lmscale
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+def to_dev_ids(J):
+    return torch.from_numpy(np.asarray(J, np.uint32).view(np.int32)).to(dev())
+
+
+def host_u32(t):
+    return t.view(torch.int32).cpu().numpy().view(np.uint32)
+
+
+# ------------------------------------------------------------------ S1
+
+UNIQUE_CASES = [
+    ("K=1", 100, np.array([7], np.uint32)),
+    ("all-equal", 100, np.full(5000, 42, np.uint32)),
+    ("all-distinct", 10000, np.random.default_rng(1).permutation(10000)[:8192].astype(np.uint32)),
+    ("max-id", 1000, np.array([999, 0, 999, 998, 0], np.uint32)),
+    ("V=1", 1, np.zeros(300, np.uint32)),
+    ("2^32-1 vocab", 2**32 - 1, np.random.default_rng(2).integers(0, 2**32 - 1, 9000,
+                                                                   dtype=np.uint64).astype(np.uint32)),
+    ("ragged-tail", 50_000, synth.zipf_ids(50_000, 1.0, 4096 * 3 + 17)),
+]
+
+
+@pytest.mark.parametrize("name,V,J", UNIQUE_CASES, ids=[c[0] for c in UNIQUE_CASES])
+def test_unique_edge_cases(lm, name, V, J):
+    ctx = lm.Context(V, len(J), 4)
+    uniq, counts, inverse = ctx.unique(to_dev_ids(J))
+    torch.cuda.synchronize()
+    ou, oc, oi = oracle.unique_local(J)
+    np.testing.assert_array_equal(host_u32(uniq), ou)
+    np.testing.assert_array_equal(counts.cpu().numpy(), oc)
+    np.testing.assert_array_equal(inverse.cpu().numpy(), oi)
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", list(synth.CONFIGS))
+def test_unique_every_config(lm, name):
+    cfg = synth.CONFIGS[name]
+    J = synth.ids_for(cfg, 0)
+    ctx = lm.Context(cfg.V, cfg.K, 4)
+    uniq, counts, inverse = ctx.unique(to_dev_ids(J))
+    ou, oc, oi = oracle.unique_local(J)
+    np.testing.assert_array_equal(host_u32(uniq), ou)
+    np.testing.assert_array_equal(counts.cpu().numpy(), oc)
+    np.testing.assert_array_equal(inverse.cpu().numpy(), oi)
+    ctx.close()
+
+
+# ---------------------------------------------------- full path, small sizes
+
+def _inputs(cfg, G, mode, step=0):
+    J = [synth.ids_for(cfg, g, step) for g in range(G)]
+    Dl = [synth.grad_values(cfg.K, cfg.D, mode, rank=g, step=step) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, mode)
+    return J, Dl, E0
+
+
+def emulate(lm, cfg, G, J, Dl, E_dev, lr):
+    """G ranks on one GPU through the staged ABI (NO_COMM context)."""
+    ctx = lm.Context(cfg.V, cfg.K, cfg.D, world=G, rank=0, flags=lm.FLAG_NO_COMM)
+    I = to_dev_ids(np.concatenate(J))                     # emulated all-gather
+    Mhat = None
+    per_rank = []
+    for g in range(G):
+        ctx.unique(to_dev_ids(J[g]), want_outputs=False)
+        ctx.global_unique(I)
+        ctx.scatter_expand(Dl[g].to(dev()))
+        sg = ctx.sparse_grad()
+        maps = ctx.local_maps()
+        per_rank.append(dict(Jhat=host_u32(maps[0]), counts=maps[1].cpu().numpy(),
+                             inverse=maps[2][:cfg.K].cpu().numpy(), l2g=maps[3].cpu().numpy(),
+                             M=sg.rows.cpu().numpy().copy()))
+        Mhat = sg.rows.clone() if Mhat is None else Mhat + sg.rows   # emulated all-reduce
+    ids = sg.ids.clone()
+    ctx.apply_update(E_dev, lm.SparseGrad.from_tensors(ids, Mhat), lr)
+    torch.cuda.synchronize()
+    out = dict(Ihat=host_u32(ids), Mhat=Mhat.cpu().numpy(), ranks=per_rank, E=E_dev.cpu().numpy())
+    ctx.close()
+    return out
+
+
+@pytest.mark.parametrize("mode", ["int", "pos", "signed"])
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_tiny_emulated_every_output(lm, mode, G):
+    cfg = synth.CONFIGS["tiny"]
+    lr = synth.default_lr(mode)
+    J, Dl, E0 = _inputs(cfg, G, mode)
+    got = emulate(lm, cfg, G, J, Dl, E0.to(dev()), lr)
+    Eo = E0.numpy().copy()
+    ref = oracle.sync_unique(J, [d.numpy() for d in Dl], Eo, lr)
+    np.testing.assert_array_equal(got["Ihat"], ref["Ihat"])
+    for g in range(G):
+        r, o = got["ranks"][g], ref["ranks"][g]
+        np.testing.assert_array_equal(r["Jhat"], o["Jhat"])
+        np.testing.assert_array_equal(r["counts"], o["counts"])
+        np.testing.assert_array_equal(r["inverse"], o["inverse"])
+        np.testing.assert_array_equal(r["l2g"], o["l2g"])
+        # M_g: zero rows exactly zero, present rows within tolerance
+        absent = np.setdiff1d(np.arange(ref["Ug"]), o["l2g"])
+        assert np.all(r["M"][absent] == 0.0)
+        check_rows(r["M"], ref["M"][g], oracle.abs_scale([J[g]], [Dl[g].numpy()], ref["Ihat"]),
+                   mode, f"M_{g}")
+    A = oracle.abs_scale(J, [d.numpy() for d in Dl], ref["Ihat"])
+    check_rows(got["Mhat"], ref["Mhat64"], A, mode, "Mhat")
+    E0n = E0.numpy()
+    touched = ref["Ihat"].astype(np.int64)
+    scaleE = np.abs(E0n[touched]) + lr * A
+    check_rows(got["E"][touched], Eo[touched].astype(np.float64) if mode == "int" else
+               (E0n[touched].astype(np.float64) - lr * ref["Mhat64"]), scaleE,
+               "int" if mode == "int" else "signed", "E rows")
+    untouched = np.setdiff1d(np.arange(cfg.V), touched)
+    np.testing.assert_array_equal(got["E"][untouched], E0n[untouched])
+
+
+@pytest.mark.parametrize("D", [1, 3, 64, 100, 4096])
+def test_odd_dims_and_wide_rows(lm, D):
+    cfg = synth.Config("odd", V=3000, K=2500, D=D)
+    mode = "int"
+    J, Dl, E0 = _inputs(cfg, 2, mode)
+    got = emulate(lm, cfg, 2, J, Dl, E0.to(dev()), 2.0 ** -4)
+    Eo = E0.numpy().copy()
+    ref = oracle.sync_unique(J, [d.numpy() for d in Dl], Eo, 2.0 ** -4)
+    np.testing.assert_array_equal(got["Ihat"], ref["Ihat"])
+    np.testing.assert_array_equal(got["Mhat"], ref["Mhat"])
+    np.testing.assert_array_equal(got["E"], Eo)
+
+
+def test_world1_collective_equals_oracle(lm):
+    cfg = synth.CONFIGS["tiny"].with_(G=1)
+    for mode in ("int", "signed"):
+        lr = synth.default_lr(mode)
+        J, Dl, E0 = _inputs(cfg, 1, mode)
+        ctx = lm.Context(cfg.V, cfg.K, cfg.D)
+        E = E0.to(dev())
+        sg = ctx.step(to_dev_ids(J[0]), Dl[0].to(dev()), E, lr)
+        torch.cuda.synchronize()
+        Eo = E0.numpy().copy()
+        ref = oracle.sync_unique(J, [Dl[0].numpy()], Eo, lr)
+        np.testing.assert_array_equal(host_u32(sg.ids), ref["Ihat"])
+        A = oracle.abs_scale(J, [Dl[0].numpy()], ref["Ihat"])
+        check_rows(sg.rows.cpu().numpy(), ref["Mhat64"], A, mode, "Mhat")
+        if mode == "int":
+            np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+        ctx.close()
+
+
+def test_deterministic_run_to_run(lm):
+    cfg = synth.CONFIGS["1b"]
+    J = to_dev_ids(synth.ids_for(cfg, 0))
+    Dg = synth.grad_values(cfg.K, cfg.D, "signed", device=dev())
+    ctx = lm.Context(cfg.V, cfg.K, cfg.D)
+    a = ctx.sync(J, Dg).rows.clone()
+    b = ctx.sync(J, Dg).rows.clone()
+    assert torch.equal(a, b)
+    ctx.close()
+
+
+def test_id_out_of_range_reported(lm):
+    ctx = lm.Context(100, 64, 8)
+    ids = to_dev_ids(np.array([1, 2, 100, 3], np.uint32))
+    g = torch.ones(4, 8, device=dev())
+    with pytest.raises(lm.LmscaleError) as e:
+        ctx.sync(ids, g)
+    assert e.value.status == lm.ID_RANGE
+    # the context stays usable
+    sg = ctx.sync(to_dev_ids(np.array([1, 2, 2, 3], np.uint32)), g)
+    assert sg.num_unique == 3
+    with pytest.raises(lm.LmscaleError):
+        ctx.sync(to_dev_ids(np.arange(65, dtype=np.uint32)), torch.ones(65, 8, device=dev()))
+    ctx.close()
+
+
+def test_dense_baseline_equals_oracle(lm):
+    cfg = synth.Config("d", V=5000, K=3000, D=32)
+    for mode in ("int", "signed"):
+        lr = synth.default_lr(mode)
+        J, Dl, E0 = _inputs(cfg, 1, mode)
+        ctx = lm.Context(cfg.V, cfg.K, cfg.D)
+        E = E0.to(dev())
+        ctx.sync_dense(to_dev_ids(J[0]), Dl[0].to(dev()), E, lr)
+        torch.cuda.synchronize()
+        Eo = oracle.sync_dense(J, [Dl[0].numpy()], E0.numpy().copy(), lr)
+        if mode == "int":
+            np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+        else:
+            np.testing.assert_allclose(E.cpu().numpy(), Eo, rtol=0, atol=2e-5)
+        # emulated G=3 dense: concatenated (I, Delta_all) through the staged scatter
+        J3, D3, _ = _inputs(cfg, 3, mode)
+        E = E0.to(dev())
+        ctx3 = lm.Context(cfg.V, cfg.K, cfg.D, world=3, flags=lm.FLAG_NO_COMM)
+        ctx3.dense_apply(to_dev_ids(np.concatenate(J3)), torch.cat(D3).to(dev()), E, lr)
+        torch.cuda.synchronize()
+        Eo = oracle.sync_dense(J3, [d.numpy() for d in D3], E0.numpy().copy(), lr)
+        if mode == "int":
+            np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+        else:
+            np.testing.assert_allclose(E.cpu().numpy(), Eo, rtol=0, atol=2e-5)
+        ctx.close()
+        ctx3.close()
+
+
+def test_host_step_equals_device_step(lm):
+    cfg = synth.CONFIGS["tiny"].with_(G=1)
+    J, Dl, E0 = _inputs(cfg, 1, "signed")
+    ctx = lm.Context(cfg.V, cfg.K, cfg.D)
+    E1 = E0.to(dev())
+    ctx.step(to_dev_ids(J[0]), Dl[0].to(dev()), E1, 0.1)
+    E2 = E0.to(dev())
+    ids_h = torch.from_numpy(J[0].view(np.int32)).pin_memory()
+    out = torch.empty(cfg.K, dtype=torch.int32).pin_memory()
+    ug = ctx.train_step_host(ids_h, Dl[0].pin_memory(), E2, 0.1, out)
+    torch.cuda.synchronize()
+    assert torch.equal(E1, E2)
+    np.testing.assert_array_equal(out[:ug].numpy().view(np.uint32), oracle.unique_global(J[0])[0])
+    ctx.close()
+
+
+def test_synth_values_identical_on_gpu():
+    for mode in ("int", "pos", "signed"):
+        a = synth.grad_values(777, 33, mode, rank=3, device=dev()).cpu()
+        b = synth.grad_values(777, 33, mode, rank=3)
+        assert torch.equal(a, b)
+    assert torch.equal(synth.table_values(999, 17, "signed", device=dev()).cpu(),
+                       synth.table_values(999, 17, "signed"))
+
+
+# ----------------------------------------------- BASELINE full sizes, G = 1
+
+def _sample_words(ref_ihat, counts_by_word, n_hot=8, n_rand=40, seed=0):
+    order = np.argsort(-counts_by_word, kind="stable")
+    hot = ref_ihat[order[:n_hot]]
+    rng = np.random.default_rng(seed)
+    rand = rng.choice(ref_ihat, size=min(n_rand, ref_ihat.size), replace=False)
+    return np.unique(np.concatenate([hot, rand, ref_ihat[-1:]]))
+
+
+@pytest.mark.parametrize("name", ["1b", "char", "amazon", "tieba"])
+def test_full_size_single_gpu(lm, name):
+    cfg = synth.CONFIGS[name]
+    mode = "signed"
+    lr = synth.default_lr(mode)
+    J = synth.ids_for(cfg, 0)
+    Dg = synth.grad_values(cfg.K, cfg.D, mode, device=dev())
+    E = synth.table_values(cfg.V, cfg.D, mode, device=dev())
+    ctx = lm.Context(cfg.V, cfg.K, cfg.D)
+    sg = ctx.sync(to_dev_ids(J), Dg)
+    rows = sg.rows.clone()
+    ids = host_u32(sg.ids)
+    ctx.apply_update(E, sg, lr)
+    torch.cuda.synchronize()
+    # integers in full
+    ou, oc, oi = oracle.unique_local(J)
+    Ihat, gcounts = oracle.unique_global(J)
+    np.testing.assert_array_equal(ids, Ihat)
+    maps = ctx.local_maps()
+    np.testing.assert_array_equal(host_u32(maps[0]), ou)
+    np.testing.assert_array_equal(maps[1].cpu().numpy(), oc)
+    np.testing.assert_array_equal(maps[2].cpu().numpy(), oi)
+    l2g, _ = oracle.remap(ou, Ihat, oi)
+    np.testing.assert_array_equal(maps[3].cpu().numpy(), l2g)
+    # sampled float rows, each from the definition
+    words = _sample_words(Ihat, gcounts)
+    slots = np.searchsorted(Ihat, words)
+    got_rows = rows[torch.from_numpy(slots).to(dev())].cpu().numpy()
+    got_E = E[torch.from_numpy(words.astype(np.int64)).to(dev())].cpu().numpy()
+    E0 = synth.table_rows(cfg.V, cfg.D, mode, words).numpy().astype(np.float64)
+    for i, w in enumerate(words):
+        pos = np.nonzero(J == w)[0]
+        d = synth.grad_rows(cfg.D, mode, pos).numpy()
+        ref, A, n = oracle.type_gradient([J[pos]], [d], w)
+        assert n == pos.size
+        check_rows(got_rows[i:i + 1], ref[None], A[None], mode, f"{name} M row of word {w}")
+        check_rows(got_E[i:i + 1], (E0[i] - lr * ref)[None], (np.abs(E0[i]) + lr * A)[None],
+                   "signed", f"{name} E row {w}")
+    if name == "char":
+        assert ids.size == 256          # saturation
+    ctx.close()
+
+
+@pytest.mark.parametrize("name,G", [("1b", 8), ("amazon", 4), ("char", 8)])
+def test_full_size_emulated_ranks_integers_and_sampled_rows(lm, name, G):
+    cfg = synth.CONFIGS[name]
+    mode = "int"
+    lr = synth.default_lr(mode)
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    ctx = lm.Context(cfg.V, cfg.K, cfg.D, world=G, flags=lm.FLAG_NO_COMM)
+    I = to_dev_ids(np.concatenate(J))
+    Ihat, gcounts = oracle.unique_global(np.concatenate(J))
+    Mhat = None
+    for g in range(G):
+        ctx.unique(to_dev_ids(J[g]), want_outputs=False)
+        ctx.global_unique(I)
+        ctx.scatter_expand(synth.grad_values(cfg.K, cfg.D, mode, rank=g, device=dev()))
+        sg = ctx.sparse_grad()
+        if g == 0:
+            np.testing.assert_array_equal(host_u32(sg.ids), Ihat)
+        maps = ctx.local_maps()
+        ou, oc, oi = oracle.unique_local(J[g])
+        l2g, _ = oracle.remap(ou, Ihat, oi)
+        np.testing.assert_array_equal(maps[3].cpu().numpy(), l2g)
+        absent = torch.ones(Ihat.size, dtype=torch.bool, device=dev())
+        absent[torch.from_numpy(l2g.astype(np.int64)).to(dev())] = False
+        assert torch.all(sg.rows[absent] == 0)
+        Mhat = sg.rows.clone() if Mhat is None else Mhat + sg.rows
+    words = _sample_words(Ihat, gcounts, n_rand=24)
+    slots = np.searchsorted(Ihat, words)
+    got = Mhat[torch.from_numpy(slots).to(dev())].cpu().numpy()
+    for i, w in enumerate(words):
+        Js, Ds = [], []
+        for g in range(G):
+            pos = np.nonzero(J[g] == w)[0]
+            Js.append(J[g][pos])
+            Ds.append(synth.grad_rows(cfg.D, mode, pos, rank=g).numpy().reshape(len(pos), cfg.D))
+        ref, A, n = oracle.type_gradient(Js, Ds, w)
+        assert n == gcounts[slots[i]]
+        check_rows(got[i:i + 1], ref[None], A[None], mode, f"{name} G={G} word {w}")
+    ctx.close()
