@@ -262,13 +262,16 @@ def main():
         st = ctx.stats()
         for k in phase:
             phase[k].append(st[k])
-        launches[0] += st["kernels_last_call"]
         info["u_local"] = st["u_local"]
 
     clk = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
                  if "CUDA_VISIBLE_DEVICES" in os.environ else local)
     clk.start()
-    ms = timed(step, args.steps, args.warmup, collect)
+    for _ in range(args.warmup):
+        step()
+    k_before = ctx.stats()["kernels_total_lo"]
+    ms = timed(step, args.steps, 0, collect)
+    launches[0] = ctx.stats()["kernels_total_lo"] - k_before
     clocks = clk.stop()
     total_ms = max_over_ranks(sum(ms), dev)
     ms_step = total_ms / args.steps

@@ -29,27 +29,19 @@ constexpr uint32_t LB_AGG = 1u << 30;
 constexpr uint32_t LB_INC = 2u << 30;
 constexpr uint32_t LB_MASK = (1u << 30) - 1u;
 
-// 128-bit streaming loads/stores.  Gradient rows are read exactly once
-// (no L1 allocation); outputs are written once.
+// 128-bit loads/stores.  Gradient rows are read exactly once (no L1
+// allocation).  The load asm is NOT volatile so the compiler may batch and
+// schedule independent loads (volatile asm pins them in program order, which
+// serialised the row loads behind their register moves).
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
   return v;
 }
-__device__ __forceinline__ float4 ld_cg(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st_v4(float4* p, float4 v) {
-  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
+__device__ __forceinline__ float4 ld_cg(const float4* p) { return __ldcg(p); }
+__device__ __forceinline__ void st_v4(float4* p, float4 v) { *p = v; }
 __device__ __forceinline__ void red_add_v4(float4* p, float4 v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w)

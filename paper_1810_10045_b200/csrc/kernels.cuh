@@ -6,19 +6,6 @@
 
 namespace lms {
 
-// Radix sort tile: 256 threads x 16 keys.
-constexpr int RS_THREADS = 256;
-constexpr int RS_ITEMS = 16;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096
-constexpr int RS_MAX_PASSES = 4;
-
-// Segment kernel tile (same shape).
-constexpr int SEG_TILE = RS_TILE;
-
-// Bitmap scan tile: 256 threads x 4 words.
-constexpr int GS_THREADS = 256;
-constexpr int GS_TILE_WORDS = GS_THREADS * 4;
-
 // Scatter-add chunk: sorted positions per warp work item.
 constexpr int SC_CHUNK = 32;
 // Zero-row group: slots per warp work item.
@@ -28,42 +15,68 @@ constexpr int SC_ZGROUP = 32;
 struct Sc1 {
   int64_t u_local;
   uint32_t err;        // bit 0: an id >= vocab seen by S1
-  uint32_t tile_ctr[RS_MAX_PASSES + 1];  // radix passes, segments
   uint32_t pad;
 };
 // Per-step device scalars of S3 (zeroed at the start of S3).
 struct Sc3 {
   int64_t u_global;
   uint32_t err;        // bit 0: an id >= vocab in I
-  uint32_t tile_ctr;   // bitmap scan
+  uint32_t pad;
 };
 
 struct SortPlan {
   int passes;
   int bits;  // digit width per pass
 };
-SortPlan make_sort_plan(uint64_t vocab);
 
-// ---- S1 -------------------------------------------------------------------
-void launch_radix_hist(const uint32_t* keys, int K, SortPlan plan, uint32_t* hist, Sc1* sc,
-                       uint32_t vocab, cudaStream_t s);
-void launch_radix_pass(int pass, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
-                       int32_t* vout, int K, SortPlan plan, const uint32_t* hist, uint32_t* lb,
-                       Sc1* sc, cudaStream_t s);
-void launch_segments(const uint32_t* sk, const int32_t* sv, int K, uint32_t vocab,
-                     uint32_t* luniq, int32_t* lstart, int32_t* segidx, int32_t* inverse,
-                     uint32_t* lbits, Sc1* sc, uint32_t* lb, int64_t* nu_out, cudaStream_t s);
+// ---- cooperative S1 / S3 (coop.cu) -----------------------------------------
+constexpr int CO_THREADS = 512;
+constexpr int CO_ITEMS = 8;
+constexpr int CO_TILE = CO_THREADS * CO_ITEMS;  // 4096 keys per tile
+constexpr int CO_MAX_BITS = 11;                 // <= 2048 digits per pass
+constexpr int CO_HOTW = 2048;                   // shared-memory bitmap words in S3
+
+struct S1Args {
+  const uint32_t* ids;
+  int K;
+  uint32_t vocab;
+  int passes, bits;
+  uint32_t *ka, *kb;
+  int32_t *va, *vb;
+  uint32_t* cT;  // [passes][1 << bits][ntp] digit-major per-tile counts
+  int ntiles, ntp;
+  uint32_t* luniq;
+  int32_t* lstart;
+  int32_t* segidx;
+  int32_t* inverse;
+  uint32_t* lbits;
+  int64_t W;
+  uint32_t* heads;  // [ntiles]
+  Sc1* sc;
+  int64_t* nu_out;
+};
+struct S3Args {
+  const uint32_t* I;
+  int64_t n;
+  uint32_t vocab;
+  uint32_t* gbits;
+  int64_t W;
+  uint32_t* wrank;
+  uint32_t* ihat;
+  uint32_t* ctot;  // [grid]
+  Sc3* sc;
+  const uint32_t* luniq;  // nullptr: skip the l2g phase
+  const Sc1* sc1;
+  int32_t* l2g;
+};
+SortPlan make_coop_plan(uint64_t vocab);
+size_t s1_smem_bytes(int bits);
+cudaError_t launch_s1(const S1Args& a, int num_sms, cudaStream_t s);
+cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s);
+
 void launch_counts_export(const int32_t* lstart, const uint32_t* luniq, const int32_t* inverse,
                           const Sc1* sc, int K, int32_t* counts, uint32_t* uniq_out,
                           int32_t* counts_out, int32_t* inverse_out, cudaStream_t s);
-
-// ---- S3 -------------------------------------------------------------------
-void launch_gbits(const uint32_t* I, int64_t n, uint32_t vocab, uint32_t* gbits, Sc3* sc,
-                  cudaStream_t s);
-void launch_gscan(const uint32_t* gbits, int64_t W, uint32_t* wrank, uint32_t* ihat, Sc3* sc,
-                  uint32_t* lb, cudaStream_t s);
-void launch_l2g(const uint32_t* luniq, const Sc1* sc1, int K, uint32_t vocab,
-                const uint32_t* gbits, const uint32_t* wrank, int32_t* l2g, cudaStream_t s);
 
 // ---- S4 -------------------------------------------------------------------
 struct ScatterArgs {

@@ -33,7 +33,6 @@ enum Ev {
   EV_GATHER_END,
   EV_S3_END,
   EV_JOIN,
-  EV_L2G_END,
   EV_SCATTER_END,
   EV_FIXUP_END,
   EV_AR_END,
@@ -47,7 +46,7 @@ enum Ev {
 struct lmscale_ctx {
   lmscale_config cfg;
   int num_sms = 0;
-  int64_t K = 0, W = 0, NI = 0, ucap = 0, nchunks = 0, rtiles = 0, gtiles = 0;
+  int64_t K = 0, W = 0, NI = 0, ucap = 0, nchunks = 0, ntiles_max = 0, ntp_max = 0;
   SortPlan plan{};
   cudaStream_t s_side = nullptr, s_copy = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_s1 = nullptr, ev_s3 = nullptr, ev_copy = nullptr;
@@ -57,13 +56,11 @@ struct lmscale_ctx {
   // device workspace
   void* base = nullptr;
   size_t ws_bytes = 0;
-  uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *hist, *lb_radix,
-      *lb_seg, *lb_gscan;
+  uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot;
   int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
   float *M, *partial;
   Sc1* sc1;
   Sc3* sc3;
-  size_t r1_off = 0, r1_bytes = 0, r3_off = 0, r3_bytes = 0;
   // lazily allocated
   float* grad_all = nullptr;
   uint32_t* stage_ids = nullptr;
@@ -143,51 +140,60 @@ void end_call(lmscale_ctx* c) {
   c->stats.kernels_total_lo = (int32_t)(c->kernels_total & 0x7fffffff);
 }
 
-// S1 on stream s: zero S1 state, histogram, LSD passes, run flags.
+// S1 on stream s: one cooperative launch (radix sort + run flags).
 lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t* nu_out,
                       cudaStream_t s) {
-  const int K = (int)k;
-  CK(cudaMemsetAsync((char*)ctx->base + ctx->r1_off, 0, ctx->r1_bytes, s));
-  launch_radix_hist(ids, K, ctx->plan, ctx->hist, ctx->sc1, (uint32_t)ctx->cfg.vocab, s);
+  S1Args a;
+  a.ids = ids;
+  a.K = (int)k;
+  a.vocab = (uint32_t)ctx->cfg.vocab;
+  a.passes = ctx->plan.passes;
+  a.bits = ctx->plan.bits;
+  a.ka = ctx->keys_a;
+  a.kb = ctx->keys_b;
+  a.va = ctx->vals_a;
+  a.vb = ctx->vals_b;
+  a.cT = ctx->cT;
+  a.ntiles = (int)((k + CO_TILE - 1) / CO_TILE);
+  a.ntp = (a.ntiles + 3) / 4 * 4;
+  a.luniq = ctx->luniq;
+  a.lstart = ctx->lstart;
+  a.segidx = ctx->segidx;
+  a.inverse = ctx->inverse;
+  a.lbits = ctx->lbits;
+  a.W = ctx->W;
+  a.heads = ctx->heads;
+  a.sc = ctx->sc1;
+  a.nu_out = nu_out;
+  CK(launch_s1(a, ctx->num_sms, s));
   LAUNCHED(1);
-  const uint32_t* kin = ids;
-  const int32_t* vin = nullptr;
-  uint32_t* kb[2] = {ctx->keys_a, ctx->keys_b};
-  int32_t* vb[2] = {ctx->vals_a, ctx->vals_b};
-  for (int p = 0; p < ctx->plan.passes; ++p) {
-    launch_radix_pass(p, kin, vin, kb[p & 1], vb[p & 1], K, ctx->plan, ctx->hist,
-                      ctx->lb_radix, ctx->sc1, s);
-    LAUNCHED(1);
-    kin = kb[p & 1];
-    vin = vb[p & 1];
-  }
-  ctx->sorted_keys = kin;
-  ctx->sorted_vals = vin;
-  launch_segments(kin, vin, K, (uint32_t)ctx->cfg.vocab, ctx->luniq, ctx->lstart, ctx->segidx,
-                  ctx->inverse, ctx->lbits, ctx->sc1, ctx->lb_seg, nu_out, s);
-  LAUNCHED(1);
+  ctx->sorted_keys = (a.passes & 1) ? ctx->keys_a : ctx->keys_b;
+  ctx->sorted_vals = (a.passes & 1) ? ctx->vals_a : ctx->vals_b;
   ctx->last_k = k;
   ctx->have_s1 = true;
   ctx->have_s3 = false;
   return LMSCALE_OK;
 }
 
-// S3 bitmap + scan on stream s (the l2g map is launched separately: it
-// needs S1's J^).
+// S3 on stream s: one cooperative launch (bitmap, scan, I^, U_g,
+// and the l2g map of the last S1, which must be complete on `s`).
 lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream_t s) {
-  CK(cudaMemsetAsync((char*)ctx->base + ctx->r3_off, 0, ctx->r3_bytes, s));
-  launch_gbits(I, n, (uint32_t)ctx->cfg.vocab, ctx->gbits, ctx->sc3, s);
-  LAUNCHED(1);
-  launch_gscan(ctx->gbits, ctx->W, ctx->wrank, ctx->ihat, ctx->sc3, ctx->lb_gscan, s);
+  S3Args a;
+  a.I = I;
+  a.n = n;
+  a.vocab = (uint32_t)ctx->cfg.vocab;
+  a.gbits = ctx->gbits;
+  a.W = ctx->W;
+  a.wrank = ctx->wrank;
+  a.ihat = ctx->ihat;
+  a.ctot = ctx->ctot;
+  a.sc = ctx->sc3;
+  a.luniq = ctx->luniq;
+  a.sc1 = ctx->sc1;
+  a.l2g = ctx->l2g;
+  CK(launch_s3(a, ctx->num_sms, s));
   LAUNCHED(1);
   ctx->last_n = n;
-  return LMSCALE_OK;
-}
-
-lmscale_status run_l2g(lmscale_ctx* ctx, cudaStream_t s) {
-  launch_l2g(ctx->luniq, ctx->sc1, (int)ctx->last_k, (uint32_t)ctx->cfg.vocab, ctx->gbits,
-             ctx->wrank, ctx->l2g, s);
-  LAUNCHED(1);
   ctx->have_s3 = true;
   return LMSCALE_OK;
 }
@@ -287,9 +293,9 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->NI = (int64_t)cfg->world * cfg->max_tokens;
     ctx->ucap = std::min<int64_t>(ctx->NI, cfg->vocab);
     ctx->nchunks = (ctx->K + SC_CHUNK - 1) / SC_CHUNK;
-    ctx->rtiles = (ctx->K + RS_TILE - 1) / RS_TILE;
-    ctx->gtiles = (ctx->W + GS_TILE_WORDS - 1) / GS_TILE_WORDS;
-    ctx->plan = make_sort_plan((uint64_t)cfg->vocab);
+    ctx->ntiles_max = (ctx->K + CO_TILE - 1) / CO_TILE;
+    ctx->ntp_max = (ctx->ntiles_max + 3) / 4 * 4;
+    ctx->plan = make_coop_plan((uint64_t)cfg->vocab);
     const int64_t K = ctx->K, D = cfg->dim;
     // ---- workspace layout (one allocation, 256-byte aligned sub-buffers)
     size_t off = 0;
@@ -303,16 +309,10 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)), o_counts = take(4 * K),
            o_l2g = take(4 * K), o_wrank = take(4 * ctx->W), o_I = take(4 * ctx->NI),
            o_ihat = take(4 * ctx->ucap);
-    // zero region R1: Sc1 | hist | radix look-back | segment look-back | lbits
-    ctx->r1_off = off;
-    size_t o_sc1 = take(sizeof(Sc1)), o_hist = take(4 * RS_MAX_PASSES * 256),
-           o_lbr = take(4 * (size_t)RS_MAX_PASSES * ctx->rtiles * 256),
-           o_lbs = take(4 * ctx->rtiles), o_lbits = take(4 * ctx->W);
-    ctx->r1_bytes = off - ctx->r1_off;
-    // zero region R3: Sc3 | gscan look-back | gbits
-    ctx->r3_off = off;
-    size_t o_sc3 = take(sizeof(Sc3)), o_lbg = take(4 * ctx->gtiles), o_gbits = take(4 * ctx->W);
-    ctx->r3_bytes = off - ctx->r3_off;
+    size_t o_sc3 = take(sizeof(Sc3) + sizeof(Sc1)), o_sc1 = o_sc3 + sizeof(Sc3),
+           o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
+           o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
+           o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W);
     size_t o_M = take(4 * (size_t)ctx->ucap * D);
     size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
     ctx->ws_bytes = off;
@@ -335,12 +335,11 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->I = (uint32_t*)(b + o_I);
     ctx->ihat = (uint32_t*)(b + o_ihat);
     ctx->sc1 = (Sc1*)(b + o_sc1);
-    ctx->hist = (uint32_t*)(b + o_hist);
-    ctx->lb_radix = (uint32_t*)(b + o_lbr);
-    ctx->lb_seg = (uint32_t*)(b + o_lbs);
-    ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->sc3 = (Sc3*)(b + o_sc3);
-    ctx->lb_gscan = (uint32_t*)(b + o_lbg);
+    ctx->cT = (uint32_t*)(b + o_cT);
+    ctx->heads = (uint32_t*)(b + o_heads);
+    ctx->ctot = (uint32_t*)(b + o_ctot);
+    ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
     ctx->M = (float*)(b + o_M);
     ctx->partial = (float*)(b + o_part);
@@ -427,8 +426,6 @@ lmscale_status lmscale_global_unique(lmscale_ctx* ctx, const uint32_t* gathered,
   cudaStream_t s = S(stream);
   lmscale_status st = run_s3(ctx, gathered, n, s);
   if (st) return st;
-  st = run_l2g(ctx, s);
-  if (st) return st;
   end_call(ctx);
   return LMSCALE_OK;
 }
@@ -502,37 +499,40 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
   ctx->timing_valid = false;
   ctx->update_timed = false;
   rec(ctx, EV_FORK, s);
-  // S1 on the side stream, concurrent with the ID all-gather.
-  CK(cudaEventRecord(ctx->ev_fork, s));
-  CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_fork, 0));
-  rec(ctx, EV_S1_BEGIN, ctx->s_side);
-  st = run_s1(ctx, ids, k, nullptr, ctx->s_side);
-  if (st) return st;
-  rec(ctx, EV_S1_END, ctx->s_side);
-  CK(cudaEventRecord(ctx->ev_s1, ctx->s_side));
-  // S2: all-gather of J.
   const uint32_t* I = ids;
   int64_t n = k;
   if (G > 1) {
+    // S1 on the side stream, concurrent with the S2 ID all-gather.
+    CK(cudaEventRecord(ctx->ev_fork, s));
+    CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_fork, 0));
+    rec(ctx, EV_S1_BEGIN, ctx->s_side);
+    st = run_s1(ctx, ids, k, nullptr, ctx->s_side);
+    if (st) return st;
+    rec(ctx, EV_S1_END, ctx->s_side);
+    CK(cudaEventRecord(ctx->ev_s1, ctx->s_side));
     NK(ncclAllGather(ids, ctx->I, (size_t)k, ncclUint32, ctx->comm, s));
     I = ctx->I;
     n = (int64_t)G * k;
+    rec(ctx, EV_GATHER_END, s);
+    CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
+  } else {
+    rec(ctx, EV_S1_BEGIN, s);
+    st = run_s1(ctx, ids, k, nullptr, s);
+    if (st) return st;
+    rec(ctx, EV_S1_END, s);
+    rec(ctx, EV_GATHER_END, s);
   }
-  rec(ctx, EV_GATHER_END, s);
-  // S3: I^, U_g; U_g + error flag to the host on the copy stream.
+  rec(ctx, EV_JOIN, s);
+  // S3: I^, U_g, l2g; {U_g, err, U_i} to the host on the copy stream.
   st = run_s3(ctx, I, n, s);
   if (st) return st;
   rec(ctx, EV_S3_END, s);
   CK(cudaEventRecord(ctx->ev_s3, s));
   CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_s3, 0));
-  CK(cudaMemcpyAsync(ctx->h_sc3, ctx->sc3, sizeof(Sc3), cudaMemcpyDeviceToHost, ctx->s_copy));
+  CK(cudaMemcpyAsync(ctx->h_sc3, ctx->sc3, sizeof(Sc3) + sizeof(Sc1), cudaMemcpyDeviceToHost,
+                     ctx->s_copy));
   CK(cudaEventRecord(ctx->ev_copy, ctx->s_copy));
-  // join S1, then l2g + S4.
-  CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
-  rec(ctx, EV_JOIN, s);
-  st = run_l2g(ctx, s);
-  if (st) return st;
-  rec(ctx, EV_L2G_END, s);
+  // S4: segmented scatter-add into M.
   st = run_s4(ctx, grad, s);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
@@ -541,6 +541,7 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
   const int64_t ug = ctx->h_sc3->u_global;
   ctx->last_ug = ug;
   ctx->stats.u_global = ug;
+  ctx->stats.u_local = ctx->h_sc1->u_local;
   if (ctx->h_sc3->err & 1u) {
     end_call(ctx);
     return fail(ctx, LMSCALE_ERR_ID_RANGE, "a token id >= vocab (%lld)",
@@ -673,8 +674,8 @@ lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
     if (ctx->update_timed) CK(cudaEventSynchronize(ctx->tev[EV_UPD_END]));
     st.us_dedup = 1e3 * ev_ms(ctx, EV_S1_BEGIN, EV_S1_END);
     st.us_gather = 1e3 * ev_ms(ctx, EV_FORK, EV_GATHER_END);
-    st.us_merge = 1e3 * ev_ms(ctx, EV_GATHER_END, EV_S3_END);
-    st.us_scatter = 1e3 * ev_ms(ctx, EV_L2G_END, EV_SCATTER_END);
+    st.us_merge = 1e3 * ev_ms(ctx, EV_JOIN, EV_S3_END);
+    st.us_scatter = 1e3 * ev_ms(ctx, EV_S3_END, EV_SCATTER_END);
     st.us_allreduce = 1e3 * ev_ms(ctx, EV_FIXUP_END, EV_AR_END);
     st.us_update = ctx->update_timed ? 1e3 * ev_ms(ctx, EV_UPD_BEGIN, EV_UPD_END) : -1.0;
     st.us_total = 1e3 * ev_ms(ctx, EV_FORK, ctx->update_timed ? EV_UPD_END : EV_AR_END);

@@ -49,11 +49,87 @@ struct Vec<float> {
 };
 
 constexpr int SC_THREADS = 256;
+constexpr unsigned FULL_MASK = 0xffffffffu;
 constexpr int FX_THREADS = 512;
 
 }  // namespace
 
 // ------------------------------------------------------------------- S4
+
+// One chunk of sorted positions [i0, i0 + n) for one column block.  FULL:
+// n == SC_CHUNK and the column block lies inside the row (no predicates).
+template <typename T, int NV, int UNR, bool FULL>
+__device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __restrict__ g,
+                                              T* __restrict__ M, T* __restrict__ P, int c,
+                                              int n, int col0, int C, int lane) {
+  using V = Vec<T>;
+  const int K = a.K;
+  const int i0 = c * SC_CHUNK;
+  int my_pos = 0, my_u = -1, my_slot = -1;
+  if (FULL || lane < n) {
+    my_pos = __ldg(a.perm + i0 + lane);
+    my_u = __ldg(a.segidx + i0 + lane);
+  }
+  const int prev_u = i0 > 0 ? __ldg(a.segidx + i0 - 1) : -1;
+  const int next_u = i0 + n < K ? __ldg(a.segidx + i0 + n) : -1;
+  if (FULL || lane < n) my_slot = __ldg(a.l2g + my_u);
+  const int up = __shfl_up_sync(FULL_MASK, my_u, 1);
+  const unsigned hmask = __ballot_sync(FULL_MASK, (FULL || lane < n) && (lane == 0 || my_u != up));
+  const bool split_left = __shfl_sync(FULL_MASK, my_u, 0) == prev_u;
+  const bool split_right = __shfl_sync(FULL_MASK, my_u, n - 1) == next_u;
+  T acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+  bool seg_first = true;  // the run being accumulated is the chunk's first
+  for (int p0 = 0; p0 < n; p0 += UNR) {
+    T r[UNR][NV];
+#pragma unroll
+    for (int q = 0; q < UNR; ++q) {
+      const int p = p0 + q;
+      const int pos = __shfl_sync(FULL_MASK, my_pos, p & 31);
+      const T* row = g + (size_t)pos * C;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int col = col0 + v * 32;
+        if (FULL) {
+          r[q][v] = V::ld_once(row + col);
+        } else {
+          r[q][v] = V::zero();
+          if (p < n && col < C) r[q][v] = V::ld_once(row + col);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UNR; ++q) {
+      const int p = p0 + q;
+      if (FULL || p < n) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
+        const bool last = (p == n - 1);
+        if (last || ((hmask >> (p + 1)) & 1u)) {
+          const int slot = __shfl_sync(FULL_MASK, my_slot, p);
+          T* dst;
+          if (seg_first && split_left)
+            dst = P + (size_t)(2 * c) * C;
+          else if (last && split_right)
+            dst = P + (size_t)(2 * c + 1) * C;
+          else
+            dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
+          if (dst) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const int col = col0 + v * 32;
+              if (FULL || col < C) V::st(dst + col, acc[v]);
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+          seg_first = false;
+        }
+      }
+    }
+  }
+}
 
 template <typename T, int NV, int UNR>
 __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
@@ -77,69 +153,12 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
     const int64_t unit = it / ncb;
     const int col0 = cb * 32 * NV + lane;
     if (unit < nchunks) {
-      // ---- chunk of sorted positions [i0, i0 + n)
       const int c = (int)unit;
-      const int i0 = c * SC_CHUNK;
-      const int n = min(SC_CHUNK, K - i0);
-      int my_pos = 0, my_u = -1, my_slot = -1;
-      if (lane < n) {
-        my_pos = __ldg(a.perm + i0 + lane);
-        my_u = __ldg(a.segidx + i0 + lane);
-        my_slot = __ldg(a.l2g + my_u);
-      }
-      const int prev_u = i0 > 0 ? __ldg(a.segidx + i0 - 1) : -1;
-      const int next_u = i0 + n < K ? __ldg(a.segidx + i0 + n) : -1;
-      const int up = __shfl_up_sync(FULL, my_u, 1);
-      const unsigned hmask = __ballot_sync(FULL, lane < n && (lane == 0 || my_u != up));
-      const bool split_left = __shfl_sync(FULL, my_u, 0) == prev_u;
-      const bool split_right = __shfl_sync(FULL, my_u, n - 1) == next_u;
-      T acc[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-      int seg_first = 1;  // the run being accumulated is the chunk's first
-      for (int p0 = 0; p0 < n; p0 += UNR) {
-        T r[UNR][NV];
-#pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-          const int p = p0 + q;
-          const int pos = __shfl_sync(FULL, my_pos, p & 31);
-          const T* row = g + (size_t)pos * C;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const int col = col0 + v * 32;
-            r[q][v] = (p < n && col < C) ? V::ld_once(row + col) : V::zero();
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < UNR; ++q) {
-          const int p = p0 + q;
-          if (p < n) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
-            const bool last = (p == n - 1);
-            if (last || ((hmask >> (p + 1)) & 1u)) {
-              const int slot = __shfl_sync(FULL, my_slot, p);
-              T* dst;
-              if (seg_first && split_left)
-                dst = P + (size_t)(2 * c) * C;
-              else if (last && split_right)
-                dst = P + (size_t)(2 * c + 1) * C;
-              else
-                dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
-              if (dst) {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                  const int col = col0 + v * 32;
-                  if (col < C) V::st(dst + col, acc[v]);
-                }
-              }
-#pragma unroll
-              for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-              seg_first = 0;
-            }
-          }
-        }
-      }
+      const int n = min(SC_CHUNK, K - c * SC_CHUNK);
+      if (n == SC_CHUNK && (cb + 1) * 32 * NV <= C)
+        scatter_chunk<T, NV, UNR, true>(a, g, M, P, c, n, col0, C, lane);
+      else
+        scatter_chunk<T, NV, UNR, false>(a, g, M, P, c, n, col0, C, lane);
     } else {
       // ---- zero rows: slots [r0, r0 + 32) whose word is absent on this rank
       const int64_t r0 = (unit - nchunks) * SC_ZGROUP;

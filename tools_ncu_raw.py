@@ -1,0 +1,20 @@
+"""Summarise key raw ncu metrics per kernel launch."""
+import csv, subprocess, sys
+rep = sys.argv[1]
+want = sys.argv[2:] or ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'launch__grid_size',
+        'launch__registers_per_thread', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'launch__occupancy_limit_registers', 'lts__t_bytes.sum',
+        'smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_drain_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_membar_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio']
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr = rows[0]
+for r in rows[2:]:
+    print(r[hdr.index('Kernel Name')][:60])
+    for w in want:
+        if w in hdr:
+            print(f"   {w:75s} {r[hdr.index(w)]}")
