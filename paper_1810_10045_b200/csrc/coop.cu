@@ -289,14 +289,14 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
     const bool valid = q < a.n && id < a.vocab;
     bad |= (q < a.n && !valid);
     const uint32_t w = id >> 5, b = 1u << (id & 31u);
-    if (valid && w < hotw) {
+    const bool hot = valid && w < hotw;
+    // convergent: every lane of the warp takes part in the match
+    const unsigned m = __match_any_sync(FULL, (valid && !hot) ? id : 0xffffffffu);
+    if (hot) {
       atomicOr(s_hot + w, b);
-    } else {
-      const unsigned m = __match_any_sync(FULL, valid ? id : 0xffffffffu);
-      if (valid && lane == (unsigned)(__ffs(m) - 1)) {
-        uint32_t* p = a.gbits + w;
-        if (!(__ldcg(p) & b)) atomicOr(p, b);
-      }
+    } else if (valid && lane == (unsigned)(__ffs(m) - 1)) {
+      uint32_t* p = a.gbits + w;
+      if (!(__ldcg(p) & b)) atomicOr(p, b);
     }
   }
   __syncthreads();
