@@ -31,6 +31,14 @@ constexpr int CT = CO_THREADS;
 constexpr int NW = CO_THREADS / 32;
 constexpr int IT = CO_ITEMS;
 
+__device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[i] = t;
+  }
+}
+
 // Block-wide sum (all threads get the result).
 __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* scratch) {
   uint32_t tot;
@@ -110,6 +118,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
   const int K = a.K;
   const bool single = a.ntiles <= (int)gridDim.x;
 
+  stamp(a.trace, 0);
   // phase 0: zero the local bitmap and scalars (ordered by the first grid.sync)
   for (int64_t w = (int64_t)blockIdx.x * CT + tid; w < a.W; w += (int64_t)gridDim.x * CT)
     a.lbits[w] = 0u;
@@ -141,7 +150,9 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
       warp_offsets(s_cnt, ndig, cT, a.ntp, t);
       __syncthreads();
     }
+    stamp(a.trace, 1 + 4 * p);
     grid.sync();
+    stamp(a.trace, 2 + 4 * p);
     // P2: bases from the digit-major count rows, then the stable scatter
     for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
       if (!single) {
@@ -190,7 +201,9 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
       }
       __syncthreads();
     }
+    stamp(a.trace, 3 + 4 * p);
     grid.sync();
+    stamp(a.trace, 4 + 4 * p);
     kin = kout;
     vin = vout;
   }
@@ -219,7 +232,9 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
     const uint32_t tot = block_sum(__popc(heads), s_scan);
     if (tid == 0) a.heads[t] = tot;
   }
+  stamp(a.trace, 20);
   grid.sync();
+  stamp(a.trace, 21);
   for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
     if (!single) load_sorted(t);
     uint32_t part = 0;
@@ -254,6 +269,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
     if (bad2) atomicOr(&a.sc->err, 1u);
     __syncthreads();
   }
+  stamp(a.trace, 22);
 }
 
 // --------------------------------------------------------------------- S3
@@ -265,13 +281,16 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   const int64_t gtid = (int64_t)blockIdx.x * CT + tid;
   const int64_t gthreads = (int64_t)gridDim.x * CT;
 
+  stamp(a.trace, 32);
   // phase 0: zero the bitmap and scalars
   for (int64_t w = gtid; w < a.W; w += gthreads) a.gbits[w] = 0u;
   if (gtid == 0) {
     a.sc->err = 0u;
     a.sc->u_global = 0;
   }
+  stamp(a.trace, 33);
   grid.sync();
+  stamp(a.trace, 34);
 
   // phase A: presence bits.  Words < CO_HOTW (the head of a frequency-ordered
   // vocabulary, where Zipf puts most tokens) are OR-ed in shared memory first
@@ -282,21 +301,31 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   for (int i = tid; i < CO_HOTW; i += CT) s_hot[i] = 0u;
   __syncthreads();
   bool bad = false;
-  const int64_t wbase0 = (gtid >> 5) << 5;
-  for (int64_t q0 = wbase0; q0 < a.n; q0 += gthreads) {
-    const int64_t q = q0 + lane;
-    const uint32_t id = q < a.n ? __ldcs(a.I + q) : 0xffffffffu;
-    const bool valid = q < a.n && id < a.vocab;
-    bad |= (q < a.n && !valid);
-    const uint32_t w = id >> 5, b = 1u << (id & 31u);
-    const bool hot = valid && w < hotw;
-    // convergent: every lane of the warp takes part in the match
-    const unsigned m = __match_any_sync(FULL, (valid && !hot) ? id : 0xffffffffu);
-    if (hot) {
-      atomicOr(s_hot + w, b);
-    } else if (valid && lane == (unsigned)(__ffs(m) - 1)) {
-      uint32_t* p = a.gbits + w;
-      if (!(__ldcg(p) & b)) atomicOr(p, b);
+  // 4 ids per lane per round, loads issued together; warp-uniform trip count
+  const int64_t wbase0 = (gtid >> 5) << 7;
+  for (int64_t q0 = wbase0; q0 < a.n; q0 += 4 * gthreads) {
+    uint32_t ids4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t q = q0 + e * 32 + lane;
+      ids4[e] = q < a.n ? __ldcs(a.I + q) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t q = q0 + e * 32 + lane;
+      const uint32_t id = ids4[e];
+      const bool valid = q < a.n && id < a.vocab;
+      bad |= (q < a.n && !valid);
+      const uint32_t w = id >> 5, b = 1u << (id & 31u);
+      const bool hot = valid && w < hotw;
+      // convergent: every lane of the warp takes part in the match
+      const unsigned m = __match_any_sync(FULL, (valid && !hot) ? id : 0xffffffffu);
+      if (hot) {
+        atomicOr(s_hot + w, b);
+      } else if (valid && lane == (unsigned)(__ffs(m) - 1)) {
+        uint32_t* p = a.gbits + w;
+        if (!(__ldcg(p) & b)) atomicOr(p, b);
+      }
     }
   }
   __syncthreads();
@@ -305,48 +334,47 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
     if (b && (__ldcg(a.gbits + i) & b) != b) atomicOr(a.gbits + i, b);
   }
   if (bad) atomicOr(&a.sc->err, 1u);
+  stamp(a.trace, 35);
   grid.sync();
+  stamp(a.trace, 36);
 
-  // phase B: popcounts of this CTA's word range (4 words per thread per round)
-  const int64_t per = ((a.W + gridDim.x - 1) / gridDim.x + 3) / 4 * 4;
+  // phase B: popcounts of this CTA's word range (one word per thread per round)
+  const int64_t per = (a.W + gridDim.x - 1) / gridDim.x;
   const int64_t w0 = (int64_t)blockIdx.x * per;
   const int64_t w1 = min(a.W, w0 + per);
   uint32_t cnt = 0;
-  for (int64_t w = w0 + 4 * (int64_t)tid; w < w1; w += 4 * CT)
-    for (int e = 0; e < 4; ++e)
-      if (w + e < w1) cnt += __popc(__ldcg(a.gbits + w + e));
+  for (int64_t w = w0 + tid; w < w1; w += CT) cnt += __popc(__ldcg(a.gbits + w));
   const uint32_t cta_tot = block_sum(cnt, s_scan);
   if (tid == 0) a.ctot[blockIdx.x] = cta_tot;
+  stamp(a.trace, 37);
   grid.sync();
+  stamp(a.trace, 38);
 
-  // phase C: CTA prefix, per-word ranks, ascending I^ emission
+  // phase C: CTA prefix, per-word ranks, ascending I^ emission.  Emission is
+  // warp-cooperative: for each of the warp's 32 words, lane b writes id
+  // 32w + b at rank r_w + popc(bits below b) -- one coalesced store per word.
   uint32_t part = 0;
   for (int c = tid; c < (int)blockIdx.x; c += CT) part += __ldcg(a.ctot + c);
   uint32_t run = block_sum(part, s_scan);
   if (blockIdx.x == gridDim.x - 1 && tid == 0) a.sc->u_global = run + cta_tot;
-  for (int64_t wr = w0; wr < w1; wr += 4 * CT) {
-    const int64_t w = wr + 4 * (int64_t)tid;
-    uint32_t wd[4] = {0, 0, 0, 0};
-    for (int e = 0; e < 4; ++e)
-      if (w + e < w1) wd[e] = __ldcg(a.gbits + w + e);
-    const uint32_t c = __popc(wd[0]) + __popc(wd[1]) + __popc(wd[2]) + __popc(wd[3]);
+  for (int64_t wr = w0; wr < w1; wr += CT) {
+    const int64_t w = wr + tid;
+    const uint32_t wd = w < w1 ? __ldcg(a.gbits + w) : 0u;
     uint32_t round_tot;
-    uint32_t r = run + block_excl_scan(c, s_scan, &round_tot);
-    for (int e = 0; e < 4; ++e) {
-      if (w + e < w1) {
-        a.wrank[w + e] = r;
-        uint32_t bits = wd[e];
-        while (bits) {
-          const int b = __ffs(bits) - 1;
-          a.ihat[r++] = (uint32_t)((w + e) * 32 + b);
-          bits &= bits - 1;
-        }
-      }
+    const uint32_t r = run + block_excl_scan(__popc(wd), s_scan, &round_tot);
+    if (w < w1) a.wrank[w] = r;
+    for (int src = 0; src < 32; ++src) {
+      const uint32_t bits = __shfl_sync(FULL, wd, src);
+      const uint32_t rs = __shfl_sync(FULL, r, src);
+      if ((bits >> lane) & 1u)
+        a.ihat[rs + __popc(bits & lanemask_lt())] = (uint32_t)((wr + (tid & ~31) + src) * 32 + lane);
     }
     run += round_tot;
   }
+  stamp(a.trace, 39);
   if (!a.luniq) return;
   grid.sync();
+  stamp(a.trace, 40);
 
   // phase D: l2g[u] = slot of J^[u] in I^ (S1 of this rank has completed)
   const int U = (int)a.sc1->u_local;
@@ -359,6 +387,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
     }
     a.l2g[u] = slot;
   }
+  stamp(a.trace, 41);
 }
 
 // ------------------------------------------------- counts / staged export

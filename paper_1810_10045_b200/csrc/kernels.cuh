@@ -54,6 +54,7 @@ struct S1Args {
   uint32_t* heads;  // [ntiles]
   Sc1* sc;
   int64_t* nu_out;
+  unsigned long long* trace;  // optional phase timestamps (LMSCALE_PHASE_TRACE)
 };
 struct S3Args {
   const uint32_t* I;
@@ -68,6 +69,7 @@ struct S3Args {
   const uint32_t* luniq;  // nullptr: skip the l2g phase
   const Sc1* sc1;
   int32_t* l2g;
+  unsigned long long* trace;
 };
 SortPlan make_coop_plan(uint64_t vocab);
 size_t s1_smem_bytes(int bits);

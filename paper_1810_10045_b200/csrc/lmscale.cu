@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -78,6 +79,7 @@ struct lmscale_ctx {
   int kernels_call = 0;
   int64_t kernels_total = 0;
   char err[512] = {0};
+  unsigned long long* trace = nullptr;  // LMSCALE_PHASE_TRACE diagnostics (64 stamps)
 };
 
 namespace {
@@ -165,6 +167,7 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   a.heads = ctx->heads;
   a.sc = ctx->sc1;
   a.nu_out = nu_out;
+  a.trace = ctx->trace;
   CK(launch_s1(a, ctx->num_sms, s));
   LAUNCHED(1);
   ctx->sorted_keys = (a.passes & 1) ? ctx->keys_a : ctx->keys_b;
@@ -191,6 +194,7 @@ lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream
   a.luniq = ctx->luniq;
   a.sc1 = ctx->sc1;
   a.l2g = ctx->l2g;
+  a.trace = ctx->trace;
   CK(launch_s3(a, ctx->num_sms, s));
   LAUNCHED(1);
   ctx->last_n = n;
@@ -360,6 +364,10 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       memcpy(&id, nccl_id, sizeof(id));
       NK(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
     }
+    if (getenv("LMSCALE_PHASE_TRACE")) {
+      CK(cudaMalloc(&ctx->trace, 64 * sizeof(unsigned long long)));
+      CK(cudaMemset(ctx->trace, 0, 64 * sizeof(unsigned long long)));
+    }
     ctx->stats.workspace_bytes = (int64_t)off;
     ctx->stats.us_dedup = ctx->stats.us_gather = ctx->stats.us_merge = ctx->stats.us_scatter =
         ctx->stats.us_allreduce = ctx->stats.us_update = ctx->stats.us_total = -1.0;
@@ -389,6 +397,7 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
   if (ctx->h_sc3) cudaFreeHost(ctx->h_sc3);
   if (ctx->base) cudaFree(ctx->base);
+  if (ctx->trace) cudaFree(ctx->trace);
   if (ctx->grad_all) cudaFree(ctx->grad_all);
   if (ctx->stage_ids) cudaFree(ctx->stage_ids);
   if (ctx->stage_grad) cudaFree(ctx->stage_grad);
@@ -551,6 +560,18 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
   if (G > 1 && ug > 0) NK(ncclAllReduce(ctx->M, ctx->M, (size_t)(ug * D), ncclFloat, ncclSum,
                                         ctx->comm, s));
   rec(ctx, EV_AR_END, s);
+  if (ctx->trace) {
+    cudaStreamSynchronize(s);
+    unsigned long long t[64];
+    cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[lmscale trace] S1:");
+    for (int i = 1; i <= 22; ++i)
+      if (t[i] && t[i - 1]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[0]) * 1e-3);
+    fprintf(stderr, " | S3:");
+    for (int i = 33; i <= 41; ++i)
+      if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
+    fprintf(stderr, " | S1start->S3start %.2f us\n", (t[32] - t[0]) * 1e-3);
+  }
   out->ids = ctx->ihat;
   out->rows = ctx->M;
   out->num_unique = ug;

@@ -1,0 +1,136 @@
+"""Multi-GPU parity worker (one process per GPU, launched by torchrun).
+
+Each rank runs the REAL collective path (lmscale_sync_embedding_grad with its
+own NCCL communicator: ID all-gather + U_g x D all-reduce) and then checks, on
+its own, against the CPU oracle: every rank can regenerate every other rank's
+seeded inputs (synth), so no expected value travels through the GPU path.
+Also checks that all replicas of the table are bit-identical afterwards
+ and the dense all-gather baseline.
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/mp_worker.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_1810_10045_b200 import lmscale  # noqa: E402
+from paper_1810_10045_b200.distributed import make_context  # noqa: E402
+from tests.tolerances import check_rows  # noqa: E402
+
+
+def u32(t):
+    return t.view(torch.int32).cpu().numpy().view(np.uint32)
+
+
+def table_digest(E):
+    """Bitwise digest of the table (int64 sum of the raw bits, per row block)."""
+    bits = E.view(torch.int32).to(torch.int64)
+    return torch.stack([bits.sum(), (bits * 1315423911).sum(), bits[::7].sum()])
+
+
+def check_replicas(E, what):
+    d = table_digest(E)
+    allds = [torch.empty_like(d) for _ in range(dist.get_world_size())]
+    dist.all_gather(allds, d)
+    for x in allds:
+        assert torch.equal(x, allds[0]), f"{what}: replicas differ"
+
+
+def run_small(ctx_full, cfg, mode, rank, G, dev):
+    lr = synth.default_lr(mode)
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    Dh = [synth.grad_values(cfg.K, cfg.D, mode, rank=g) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, mode)
+    ctx = make_context(cfg.V, cfg.K, cfg.D)
+    E = E0.to(dev)
+    sg = ctx.sync(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev))
+    ids, rows = u32(sg.ids), sg.rows.cpu().numpy()
+    ctx.apply_update(E, sg, lr)
+    torch.cuda.synchronize()
+    Eo = E0.numpy().copy()
+    ref = oracle.sync_unique(J, [d.numpy() for d in Dh], Eo, lr)
+    np.testing.assert_array_equal(ids, ref["Ihat"])
+    A = oracle.abs_scale(J, [d.numpy() for d in Dh], ref["Ihat"])
+    check_rows(rows, ref["Mhat64"], A, mode, f"G={G} {cfg.name} {mode} Mhat")
+    if mode == "int":
+        np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+    maps = ctx.local_maps()
+    np.testing.assert_array_equal(maps[3].cpu().numpy(), ref["ranks"][rank]["l2g"])
+    check_replicas(E, f"{cfg.name} {mode}")
+    # dense baseline on the same inputs
+    Ed = E0.to(dev)
+    ctx.sync_dense(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), Ed, lr)
+    torch.cuda.synchronize()
+    Edo = oracle.sync_dense(J, [d.numpy() for d in Dh], E0.numpy().copy(), lr)
+    if mode == "int":
+        np.testing.assert_array_equal(Ed.cpu().numpy(), Edo)
+    else:
+        np.testing.assert_allclose(Ed.cpu().numpy(), Edo, rtol=0, atol=2e-5)
+    check_replicas(Ed, f"dense {cfg.name} {mode}")
+    ctx.close()
+
+
+def run_full(cfg, rank, G, dev, n_rand=24):
+    """BASELINE full size on G real GPUs: integers in full, sampled float rows."""
+    mode = "signed"
+    lr = synth.default_lr(mode)
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    ctx = make_context(cfg.V, cfg.K, cfg.D)
+    grad = synth.grad_values(cfg.K, cfg.D, mode, rank=rank, device=dev)
+    E = synth.table_values(cfg.V, cfg.D, mode, device=dev)
+    sg = ctx.sync(torch.from_numpy(J[rank].view(np.int32)).to(dev), grad)
+    rows = sg.rows.clone()
+    ids = u32(sg.ids)
+    ctx.apply_update(E, sg, lr)
+    torch.cuda.synchronize()
+    Ihat, gcounts = oracle.unique_global(np.concatenate(J))
+    np.testing.assert_array_equal(ids, Ihat)
+    order = np.argsort(-gcounts, kind="stable")
+    rng = np.random.default_rng(rank)
+    words = np.unique(np.concatenate([Ihat[order[:6]], rng.choice(Ihat, n_rand, replace=False)]))
+    slots = np.searchsorted(Ihat, words)
+    got = rows[torch.from_numpy(slots).to(dev)].cpu().numpy()
+    gotE = E[torch.from_numpy(words.astype(np.int64)).to(dev)].cpu().numpy()
+    E0 = synth.table_rows(cfg.V, cfg.D, mode, words).numpy().astype(np.float64)
+    for i, w in enumerate(words):
+        Js, Ds = [], []
+        for g in range(G):
+            pos = np.nonzero(J[g] == w)[0]
+            Js.append(J[g][pos])
+            Ds.append(synth.grad_rows(cfg.D, mode, pos, rank=g).numpy().reshape(len(pos), cfg.D))
+        ref, A, n = oracle.type_gradient(Js, Ds, w)
+        check_rows(got[i:i + 1], ref[None], A[None], mode, f"{cfg.name} G={G} word {w}")
+        check_rows(gotE[i:i + 1], (E0[i] - lr * ref)[None], (np.abs(E0[i]) + lr * A)[None],
+                   "signed", f"{cfg.name} G={G} E row {w}")
+    check_replicas(E, f"full {cfg.name}")
+    ctx.close()
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, G = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", local)
+    which = sys.argv[1:] or ["small", "1b", "char"]
+    if "small" in which:
+        for mode in ("int", "signed"):
+            run_small(None, synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev)
+        run_small(None, synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
+    for name in ("1b", "char", "amazon", "tieba"):
+        if name in which:
+            run_full(synth.CONFIGS[name], rank, G, dev)
+    dist.barrier()
+    if rank == 0:
+        print(f"MP_OK G={G} {which}", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

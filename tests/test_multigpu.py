@@ -1,0 +1,73 @@
+"""Multi-process paths.
+
+CPU (gloo, world_size 2, 127.0.0.1): the host-side plumbing the N>1 path
+uses -- NCCL-id distribution and the max-over-ranks timing reduction.
+GPU (>= 2 devices): the real NCCL exchange through tests/mp_worker.py under
+torchrun, checked on every rank against the oracle.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    from paper_1810_10045_b200 import distributed as D
+    fake = bytes(range(128))
+    nid = D.share_nccl_id(make_id=lambda: fake)
+    assert nid == fake
+    m = D.max_over_ranks(10.0 + rank)
+    b = D.broadcast_bytes(b"x" * (rank + 1) if rank == 1 else None, src=1)
+    q.put((rank, nid == fake, m, b))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_host_plumbing():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    for rank, ok, m, b in res:
+        assert ok and m == 11.0 and b == b"xx"
+
+
+def _torchrun(n, args, timeout=900):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MP_OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_nccl_exchange_matches_oracle(n):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    _torchrun(n, ["small", "1b", "char"])

@@ -1,0 +1,27 @@
+"""Run a few exchange steps of one config with the in-kernel phase trace on.
+
+    LMSCALE_PHASE_TRACE=1 python tools/trace_step.py 1b [steps]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_1810_10045_b200 import lmscale  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "1b"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+cfg = synth.CONFIGS[name]
+dev = torch.device("cuda", 0)
+ids = torch.from_numpy(synth.ids_for(cfg, 0).view(np.int32)).to(dev)
+grad = synth.grad_values(cfg.K, cfg.D, "signed", device=dev)
+table = synth.table_values(cfg.V, cfg.D, "signed", device=dev)
+ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+for i in range(steps):
+    ctx.step(ids, grad, table, 0.1)
+    torch.cuda.synchronize()
+    st = ctx.stats()
+    print({k: round(v, 2) for k, v in st.items() if k.startswith("us_")}, file=sys.stderr)
