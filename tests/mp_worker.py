@@ -70,9 +70,12 @@ def run_small(ctx_full, cfg, mode, rank, G, dev):
     Edo = oracle.sync_dense(J, [d.numpy() for d in Dh], E0.numpy().copy(), lr)
     if mode == "int":
         np.testing.assert_array_equal(Ed.cpu().numpy(), Edo)
+        check_replicas(Ed, f"dense {cfg.name} {mode}")
     else:
+        # fp32 atomics land in a different order on every GPU, so the dense
+        # baseline's replicas agree only to rounding (the unique path above is
+        # bit-identical by construction: P:433-435)
         np.testing.assert_allclose(Ed.cpu().numpy(), Edo, rtol=0, atol=2e-5)
-    check_replicas(Ed, f"dense {cfg.name} {mode}")
     ctx.close()
 
 
