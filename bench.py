@@ -255,8 +255,7 @@ def main():
     launches = [0]
 
     def step():
-        sg = ctx.step(ids, grad, table, lr)
-        info["ug"] = sg.num_unique
+        ctx.step(ids, grad, table, lr)
 
     def collect():
         st = ctx.stats()
@@ -273,6 +272,7 @@ def main():
     ms = timed(step, args.steps, 0, collect)
     launches[0] = ctx.stats()["kernels_total_lo"] - k_before
     clocks = clk.stop()
+    info["ug"] = ctx.sparse_grad().num_unique
     total_ms = max_over_ranks(sum(ms), dev)
     ms_step = total_ms / args.steps
     tokens = world * cfg.K

@@ -189,6 +189,19 @@ LMSCALE_API lmscale_status lmscale_apply_sparse_update(lmscale_ctx* ctx, float* 
                                            const lmscale_sparse_grad* sg /* host */,
                                            float lr, void* stream);
 
+/* One whole training-step exchange, S1-S6: the collective sync
+ * of lmscale_sync_embedding_grad followed by the row update of
+ * lmscale_apply_sparse_update on `table` (vocab x dim, in place), in one call.
+ * With world == 1 and num_unique_out == NULL the host never waits: S6 reads
+ * U_g on the device, so the call returns as soon as the kernels are enqueued.
+ * num_unique_out (host, may be NULL) receives U_g (forces a host sync point).
+ * Collective when world > 1; errors as lmscale_sync_embedding_grad (with
+ * world == 1 and no host sync, ID_RANGE surfaces at the next
+ * lmscale_get_sparse_grad). */
+LMSCALE_API lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* grad,
+                                        int64_t k, float* table, float lr,
+                                        int64_t* num_unique_out /* host, or NULL */, void* stream);
+
 /* S0, the comparison path: all-gather ids and the k x dim grad
  * rows of every rank (Theta(G K D) bytes), then apply all G*k row updates
  * table[I[q]] -= lr * Delta_all[q] with 128-bit vector atomics (the paper's

@@ -102,8 +102,10 @@ void launch_scatter(const ScatterArgs& a, cudaStream_t s);
 void launch_fixup(const ScatterArgs& a, cudaStream_t s);
 
 // ---- S6 / S0 --------------------------------------------------------------
+// n_dev != nullptr: the row count is read on the device (min(n, *n_dev)); n
+// is then the capacity that sizes the grid.
 void launch_update(float* table, int D, const uint32_t* ids, const float* rows, int64_t n,
-                   float lr, int num_sms, cudaStream_t s);
+                   const int64_t* n_dev, float lr, int num_sms, cudaStream_t s);
 void launch_dense(float* table, int D, const uint32_t* ids, const float* grad, int64_t n,
                   float lr, uint32_t vocab, int num_sms, cudaStream_t s);
 

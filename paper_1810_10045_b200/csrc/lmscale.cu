@@ -75,6 +75,7 @@ struct lmscale_ctx {
   const uint32_t* sorted_keys = nullptr;
   const int32_t* sorted_vals = nullptr;
   int64_t last_ug = 0;
+  bool have_pending_ug = false;  // last step did not read U_g back to the host
   lmscale_stats stats{};
   int kernels_call = 0;
   int64_t kernels_total = 0;
@@ -493,12 +494,18 @@ lmscale_status lmscale_get_local_maps(lmscale_ctx* ctx, const uint32_t** uniq,
 
 // ----------------------------------------------------------- collective path
 
-lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids,
-                                           const float* grad, int64_t k,
-                                           lmscale_sparse_grad* out, void* stream) {
+}  // extern "C"
+
+namespace {
+// S1-S5 (+ S6 when table != nullptr).  With G == 1 and table != nullptr the
+// host never waits: S6 reads U_g on the device.  need_host_ug forces the
+// {U_g, err, U_i} readback (always done for G > 1: NCCL's count is a host value).
+lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* grad, int64_t k,
+                         float* table, float lr, bool need_host_ug, lmscale_sparse_grad* out,
+                         void* stream) {
   lmscale_status st = check_ids_args(ctx, ids, k);
   if (st) return st;
-  if (!grad || !out) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad/out is NULL");
+  if (!grad) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad is NULL");
   if ((ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
     return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "collective call on a NO_COMM context");
   begin_call(ctx);
@@ -545,8 +552,28 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
   st = run_s4(ctx, grad, s);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
+  if (G == 1 && table && !need_host_ug) {
+    // S6 straight away with the device-side count: no host round trip.
+    rec(ctx, EV_AR_END, s);
+    rec(ctx, EV_UPD_BEGIN, s);
+    launch_update(table, (int)D, ctx->ihat, ctx->M, ctx->ucap, &ctx->sc3->u_global, lr,
+                  ctx->num_sms, s);
+    LAUNCHED(1);
+    rec(ctx, EV_UPD_END, s);
+    ctx->update_timed = timing(ctx);
+    ctx->timing_valid = timing(ctx);
+    ctx->have_pending_ug = true;
+    if (out) {
+      out->ids = ctx->ihat;
+      out->rows = ctx->M;
+      out->num_unique = -1;
+    }
+    end_call(ctx);
+    return LMSCALE_OK;
+  }
   // host learns U_g (hidden behind the scatter kernel)
   CK(cudaEventSynchronize(ctx->ev_copy));
+  ctx->have_pending_ug = false;
   const int64_t ug = ctx->h_sc3->u_global;
   ctx->last_ug = ug;
   ctx->stats.u_global = ug;
@@ -560,6 +587,13 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
   if (G > 1 && ug > 0) NK(ncclAllReduce(ctx->M, ctx->M, (size_t)(ug * D), ncclFloat, ncclSum,
                                         ctx->comm, s));
   rec(ctx, EV_AR_END, s);
+  if (table) {
+    rec(ctx, EV_UPD_BEGIN, s);
+    launch_update(table, (int)D, ctx->ihat, ctx->M, ug, nullptr, lr, ctx->num_sms, s);
+    if (ug > 0) LAUNCHED(1);
+    rec(ctx, EV_UPD_END, s);
+    ctx->update_timed = timing(ctx);
+  }
   if (ctx->trace) {
     cudaStreamSynchronize(s);
     unsigned long long t[64];
@@ -572,9 +606,11 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
       if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
     fprintf(stderr, " | S1start->S3start %.2f us\n", (t[32] - t[0]) * 1e-3);
   }
-  out->ids = ctx->ihat;
-  out->rows = ctx->M;
-  out->num_unique = ug;
+  if (out) {
+    out->ids = ctx->ihat;
+    out->rows = ctx->M;
+    out->num_unique = ug;
+  }
   ctx->stats.bytes_ids_gathered = 4 * (int64_t)(G - 1) * k;
   ctx->stats.bytes_grad_allreduce = G > 1 ? 4 * ug * D : 0;
   ctx->stats.bytes_scatter = 4 * k * D + 4 * ug * D;
@@ -582,6 +618,27 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
   ctx->timing_valid = timing(ctx);
   end_call(ctx);
   return LMSCALE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids,
+                                           const float* grad, int64_t k,
+                                           lmscale_sparse_grad* out, void* stream) {
+  if (ctx && !out) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "out is NULL");
+  return step_impl(ctx, ids, grad, k, nullptr, 0.f, true, out, stream);
+}
+
+lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* grad, int64_t k,
+                            float* table, float lr, int64_t* num_unique_out, void* stream) {
+  if (ctx && !table) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "table is NULL");
+  lmscale_sparse_grad sg;
+  lmscale_status st =
+      step_impl(ctx, ids, grad, k, table, lr, num_unique_out != nullptr, &sg, stream);
+  if (st == LMSCALE_OK && num_unique_out) *num_unique_out = sg.num_unique;
+  return st;
 }
 
 lmscale_status lmscale_apply_sparse_update(lmscale_ctx* ctx, float* table,
@@ -594,7 +651,8 @@ lmscale_status lmscale_apply_sparse_update(lmscale_ctx* ctx, float* table,
   begin_call(ctx);
   cudaStream_t s = S(stream);
   rec(ctx, EV_UPD_BEGIN, s);
-  launch_update(table, (int)ctx->cfg.dim, sg->ids, sg->rows, sg->num_unique, lr, ctx->num_sms, s);
+  launch_update(table, (int)ctx->cfg.dim, sg->ids, sg->rows, sg->num_unique, nullptr, lr,
+                ctx->num_sms, s);
   if (sg->num_unique > 0) LAUNCHED(1);
   rec(ctx, EV_UPD_END, s);
   ctx->update_timed = timing(ctx);
@@ -671,13 +729,8 @@ lmscale_status lmscale_train_step_host(lmscale_ctx* ctx, const uint32_t* ids_hos
   CK(cudaMemcpyAsync(ctx->stage_ids, ids_host, 4 * (size_t)k, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->stage_grad, grad_host, 4 * (size_t)k * D, cudaMemcpyHostToDevice, s));
   lmscale_sparse_grad sg;
-  st = lmscale_sync_embedding_grad(ctx, ctx->stage_ids, ctx->stage_grad, k, &sg, stream);
+  st = step_impl(ctx, ctx->stage_ids, ctx->stage_grad, k, table, lr, true, &sg, stream);
   if (st) return st;
-  int kc = ctx->kernels_call;
-  st = lmscale_apply_sparse_update(ctx, table, &sg, lr, stream);
-  if (st) return st;
-  ctx->kernels_call += kc;
-  ctx->stats.kernels_last_call = ctx->kernels_call;
   if (ids_out_host && sg.num_unique > 0)
     CK(cudaMemcpyAsync(ids_out_host, sg.ids, 4 * (size_t)sg.num_unique, cudaMemcpyDeviceToHost,
                        s));

@@ -327,8 +327,9 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_update(float* __restrict__ table, int D,
                                                 const uint32_t* __restrict__ ids,
                                                 const float* __restrict__ rows, int64_t n,
-                                                float lr) {
+                                                const int64_t* __restrict__ n_dev, float lr) {
   using V = Vec<T>;
+  if (n_dev) n = min(n, *n_dev);  // device-side count (no host round trip)
   const int C = D / V::W;
   const int lane = (int)lane_id();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -353,16 +354,16 @@ __global__ void __launch_bounds__(256) k_update(float* __restrict__ table, int D
 }
 
 void launch_update(float* table, int D, const uint32_t* ids, const float* rows, int64_t n,
-                   float lr, int num_sms, cudaStream_t s) {
+                   const int64_t* n_dev, float lr, int num_sms, cudaStream_t s) {
   if (n <= 0) return;
   int64_t blocks = (n + 7) / 8;
   const int64_t cap = (int64_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)rows % 16 == 0;
   if (v4)
-    k_update<float4><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, lr);
+    k_update<float4><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, n_dev, lr);
   else
-    k_update<float><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, lr);
+    k_update<float><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, n_dev, lr);
 }
 
 // ------------------------------------------------------------------- S0

@@ -73,6 +73,7 @@ _sync = _sig("lmscale_sync_embedding_grad", _S,
              [_P, _P, _P, _i64, ctypes.POINTER(SparseGradC), _P])
 _apply = _sig("lmscale_apply_sparse_update", _S,
               [_P, _P, ctypes.POINTER(SparseGradC), ctypes.c_float, _P])
+_step = _sig("lmscale_step", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, ctypes.POINTER(_i64), _P])
 _dense = _sig("lmscale_sync_dense_baseline", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, _P])
 _dense_apply = _sig("lmscale_dense_apply", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, _P])
 _host_step = _sig("lmscale_train_step_host", _S,
@@ -85,7 +86,7 @@ _version = _sig("lmscale_version", ctypes.c_char_p, [])
 EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_unique",
             "lmscale_global_unique", "lmscale_scatter_expand", "lmscale_get_sparse_grad",
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
-            "lmscale_apply_sparse_update", "lmscale_sync_dense_baseline",
+            "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
             "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
 
@@ -262,10 +263,18 @@ class Context:
         self._check(_apply(self._h, _ptr(table), ctypes.byref(sg.c), float(lr), _stream(stream)),
                     "lmscale_apply_sparse_update")
 
-    def step(self, ids, grad, table, lr, stream=None) -> SparseGrad:
-        sg = self.sync(ids, grad, stream)
-        self.apply_update(table, sg, lr, stream)
-        return sg
+    def step(self, ids, grad, table, lr, want_num_unique=False, stream=None):
+        """S1-S6 in one C call (lmscale_step).  Returns U_g if asked (that
+        forces a host sync), else None -- with world == 1 the call then
+        returns as soon as the kernels are enqueued."""
+        ids = self._ids(ids)
+        assert grad.dtype == torch.float32 and grad.is_cuda and grad.is_contiguous()
+        assert table.dtype == torch.float32 and table.is_cuda and table.is_contiguous()
+        n = _i64(-1)
+        self._check(_step(self._h, _ptr(ids), _ptr(grad), ids.numel(), _ptr(table), float(lr),
+                          ctypes.byref(n) if want_num_unique else None, _stream(stream)),
+                    "lmscale_step")
+        return int(n.value) if want_num_unique else None
 
     def sync_dense(self, ids, grad, table, lr, stream=None):
         """S0: dense all-gather baseline, table updated in place."""

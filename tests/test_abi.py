@@ -18,8 +18,8 @@ def declared_functions():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_1810_10045_b200 import _build
-    path = _build.build()
+    import __graft_entry__
+    path = __graft_entry__._load_builder().build()
     return ctypes.CDLL(path), path
 
 

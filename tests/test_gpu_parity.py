@@ -165,8 +165,16 @@ def test_world1_collective_equals_oracle(lm):
         J, Dl, E0 = _inputs(cfg, 1, mode)
         ctx = lm.Context(cfg.V, cfg.K, cfg.D)
         E = E0.to(dev())
-        sg = ctx.step(to_dev_ids(J[0]), Dl[0].to(dev()), E, lr)
+        sg = ctx.sync(to_dev_ids(J[0]), Dl[0].to(dev()))
+        ctx.apply_update(E, sg, lr)
         torch.cuda.synchronize()
+        # the fused one-call step (device-side U_g at world 1) gives the same table
+        E2 = E0.to(dev())
+        assert ctx.step(to_dev_ids(J[0]), Dl[0].to(dev()), E2, lr) is None
+        torch.cuda.synchronize()
+        assert torch.equal(E, E2)
+        assert ctx.step(to_dev_ids(J[0]), Dl[0].to(dev()), E0.to(dev()), lr,
+                        want_num_unique=True) == sg.num_unique
         Eo = E0.numpy().copy()
         ref = oracle.sync_unique(J, [Dl[0].numpy()], Eo, lr)
         np.testing.assert_array_equal(host_u32(sg.ids), ref["Ihat"])
