@@ -59,7 +59,10 @@ struct lmscale_ctx {
   size_t ws_bytes = 0;
   uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot;
   int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
-  float *M, *partial;
+  float* M = nullptr;
+  float* partial;
+  bool m_nccl = false;
+  void* m_reg = nullptr;
   Sc1* sc1;
   Sc3* sc3;
   // lazily allocated
@@ -318,7 +321,9 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
            o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
            o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W);
-    size_t o_M = take(4 * (size_t)ctx->ucap * D);
+    // M lives in its own allocation: with a communicator it comes from
+    // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
+    const size_t m_bytes = align_up(4 * (size_t)ctx->ucap * D, 1 << 21);
     size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
     ctx->ws_bytes = off;
     if (cudaMalloc(&ctx->base, off) != cudaSuccess) {
@@ -346,7 +351,6 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->ctot = (uint32_t*)(b + o_ctot);
     ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
-    ctx->M = (float*)(b + o_M);
     ctx->partial = (float*)(b + o_part);
     CK(cudaMemset(ctx->base, 0, off));
     CK(cudaHostAlloc((void**)&ctx->h_sc3, sizeof(Sc3) + sizeof(Sc1), cudaHostAllocDefault));
@@ -364,7 +368,21 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       ncclUniqueId id;
       memcpy(&id, nccl_id, sizeof(id));
       NK(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
+      void* m = nullptr;
+      if (ncclMemAlloc(&m, m_bytes) != ncclSuccess)
+        return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(%zu) failed", m_bytes);
+      ctx->M = (float*)m;
+      ctx->m_nccl = true;
+      if (!getenv("LMSCALE_NO_REGISTER"))
+        NK(ncclCommRegister(ctx->comm, ctx->M, m_bytes, &ctx->m_reg));
+    } else {
+      if (cudaMalloc((void**)&ctx->M, m_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(%zu) failed", m_bytes);
+      }
     }
+    CK(cudaMemset(ctx->M, 0, m_bytes));
+    off += m_bytes;
     if (getenv("LMSCALE_PHASE_TRACE")) {
       CK(cudaMalloc(&ctx->trace, 64 * sizeof(unsigned long long)));
       CK(cudaMemset(ctx->trace, 0, 64 * sizeof(unsigned long long)));
@@ -387,6 +405,13 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
+  if (ctx->m_reg) ncclCommDeregister(ctx->comm, ctx->m_reg);
+  if (ctx->M) {
+    if (ctx->m_nccl)
+      ncclMemFree(ctx->M);
+    else
+      cudaFree(ctx->M);
+  }
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (int i = 0; i < EV_COUNT; ++i)
     if (ctx->tev[i]) cudaEventDestroy(ctx->tev[i]);

@@ -1,0 +1,17 @@
+"""One-line summaries of bench JSON lines found in the given log files."""
+import json
+import sys
+
+for f in sys.argv[1:]:
+    for line in open(f):
+        line = line.strip()
+        if not line.startswith("{"):
+            continue
+        d = json.loads(line)
+        ph = {k.replace("us_", ""): round(v, 1) for k, v in (d.get("phases_us_median") or {}).items()}
+        dn = d.get("dense_baseline") or {}
+        print(f"{f}: {d['config']['workload']} N={d['n_gpus']} {d['value']/1e6:.1f} Mtok/s "
+              f"{d.get('us_per_step', 0):.1f} us/step U_g={d.get('U_global')} phases={ph} "
+              f"S4frac={d.get('roofline', {}).get('frac', 0):.3f} "
+              f"dense_us={1e3*dn.get('ms_per_step', 0):.1f} speedup={dn.get('speedup_unique_vs_dense', 0):.2f} "
+              f"gate={dn.get('gate_0.8x', 0):.2f} e2e={((d.get('e2e') or {}).get('value') or 0)/1e6:.1f}M")
