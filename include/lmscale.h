@@ -103,6 +103,9 @@ typedef struct {
   int64_t workspace_bytes;     /* device bytes owned by the context */
   int32_t kernels_last_call;   /* kernels this library launched in the last call */
   int32_t kernels_total_lo;    /* running count of launched kernels (low 31 bits) */
+  int32_t fused_s5_s6;         /* 1: the last step ran S5+S6 as one NVLS multicast kernel
+                                  (us_allreduce then times that kernel, us_update ~ 0) */
+  int32_t nvls_available;      /* 1: the context has the multicast window (world > 1) */
 } lmscale_stats;
 
 /* ------------------------------------------------------------------ setup */

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 namespace lms {
 
@@ -108,5 +109,15 @@ void launch_update(float* table, int D, const uint32_t* ids, const float* rows, 
                    const int64_t* n_dev, float lr, int num_sms, cudaStream_t s);
 void launch_dense(float* table, int D, const uint32_t* ids, const float* grad, int64_t n,
                   float lr, uint32_t vocab, int num_sms, cudaStream_t s);
+
+// ---- S5+S6 fused over NVLS multicast (nvls.cu) ------------------------------
+struct NvlsState;
+// Collective (every rank, same order): window-register M and create a device
+// communicator with a multimem mapping.  nullptr (+ err) if unsupported.
+NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char* err,
+                       size_t errlen);
+void nvls_destroy(ncclComm_t comm, NvlsState* st);
+void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
+                        const float* M, int D, float lr, int rank, int world, cudaStream_t s);
 
 }  // namespace lms

@@ -63,6 +63,8 @@ struct lmscale_ctx {
   float* partial;
   bool m_nccl = false;
   void* m_reg = nullptr;
+  NvlsState* nvls = nullptr;   // fused S5+S6 available
+  char nvls_why[256] = {0};    // why not, when it is not
   Sc1* sc1;
   Sc3* sc3;
   // lazily allocated
@@ -79,6 +81,7 @@ struct lmscale_ctx {
   const int32_t* sorted_vals = nullptr;
   int64_t last_ug = 0;
   bool have_pending_ug = false;  // last step did not read U_g back to the host
+  bool fused_last = false;       // last step used the fused NVLS S5+S6 kernel
   lmscale_stats stats{};
   int kernels_call = 0;
   int64_t kernels_total = 0;
@@ -373,8 +376,17 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
         return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(%zu) failed", m_bytes);
       ctx->M = (float*)m;
       ctx->m_nccl = true;
-      if (!getenv("LMSCALE_NO_REGISTER"))
+      // Fused S5+S6 over NVLS needs a symmetric window with a multicast
+      // mapping; without it, M is registered for NCCL's zero-copy all-reduce.
+      char why[256] = {0};
+      if (!getenv("LMSCALE_NO_NVLS"))
+        ctx->nvls = nvls_create(ctx->comm, ctx->M, m_bytes, ctx->num_sms, why, sizeof(why));
+      else
+        snprintf(why, sizeof(why), "LMSCALE_NO_NVLS set");
+      if (!ctx->nvls) {
+        snprintf(ctx->nvls_why, sizeof(ctx->nvls_why), "%s", why);
         NK(ncclCommRegister(ctx->comm, ctx->M, m_bytes, &ctx->m_reg));
+      }
     } else {
       if (cudaMalloc((void**)&ctx->M, m_bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -405,6 +417,7 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
+  if (ctx->nvls) nvls_destroy(ctx->comm, ctx->nvls);
   if (ctx->m_reg) ncclCommDeregister(ctx->comm, ctx->m_reg);
   if (ctx->M) {
     if (ctx->m_nccl)
@@ -577,6 +590,38 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   st = run_s4(ctx, grad, s);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
+  if (G > 1 && table && ctx->nvls) {
+    // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
+    launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
+                       ctx->cfg.rank, G, s);
+    LAUNCHED(1);
+    rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
+    rec(ctx, EV_UPD_BEGIN, s);
+    rec(ctx, EV_UPD_END, s);
+    ctx->update_timed = timing(ctx);
+    ctx->timing_valid = timing(ctx);
+    ctx->fused_last = true;
+    int64_t ug = -1;
+    if (need_host_ug) {
+      CK(cudaEventSynchronize(ctx->ev_copy));
+      ug = ctx->h_sc3->u_global;
+      ctx->stats.u_global = ug;
+      ctx->stats.u_local = ctx->h_sc1->u_local;
+      if (ctx->h_sc3->err & 1u) {
+        end_call(ctx);
+        return fail(ctx, LMSCALE_ERR_ID_RANGE, "a token id >= vocab (%lld)",
+                    (long long)ctx->cfg.vocab);
+      }
+    }
+    if (out) {
+      out->ids = ctx->ihat;
+      out->rows = nullptr;  // M was consumed by the fused update
+      out->num_unique = ug;
+    }
+    end_call(ctx);
+    return LMSCALE_OK;
+  }
+  ctx->fused_last = false;
   if (G == 1 && table && !need_host_ug) {
     // S6 straight away with the device-side count: no host round trip.
     rec(ctx, EV_AR_END, s);
@@ -779,6 +824,8 @@ lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
     st.us_update = ctx->update_timed ? 1e3 * ev_ms(ctx, EV_UPD_BEGIN, EV_UPD_END) : -1.0;
     st.us_total = 1e3 * ev_ms(ctx, EV_FORK, ctx->update_timed ? EV_UPD_END : EV_AR_END);
   }
+  st.fused_s5_s6 = ctx->fused_last ? 1 : 0;
+  st.nvls_available = ctx->nvls ? 1 : 0;
   *out = st;
   return LMSCALE_OK;
 }

@@ -1,0 +1,213 @@
+// nvls.cu -- S5 + S6 fused over NVLink SHARP multicast (NVLS): the all-reduce
+// of M (step 6) and the duplicate-free row update of E (step 7,
+// P:421) in ONE kernel, through NCCL 2.28's device API.
+//
+// M (U_g x D, one copy per rank) sits in an NCCL symmetric window with a
+// multicast (multimem) mapping on the NVSwitch.  Rank i owns the slice of rows
+// [U_g*i/G, U_g*(i+1)/G):
+//   1. LSA barrier: every rank's M_g is complete (S4 ran before on each rank);
+//   2. for each owned row: multimem.ld_reduce (the switch sums the G copies),
+//      e' = fma(-lr, m, E[I^[r]]) written to the local E, and multimem.st of e'
+//      into M[r] of every rank (the owner's result is the only one, so the
+//      replicas stay bit-identical);
+//   3. LSA barrier: all broadcasts landed;
+//   4. for every row of the other slices: E[I^[r]] = M[r] (local copy).
+// Per GPU that is ~1x the payload each way over NVLink (a ring all-reduce
+// moves 2(G-1)/G x), no separate 12*U_g*D update pass, and no host round trip:
+// U_g is read on the device.  Barriers are per CTA index: CTA k of every rank
+// handles the same relative rows of every slice, so CTA k only has to meet the
+// CTAs k of the other ranks.
+#include <nccl.h>
+#include <nccl_device.h>
+
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace lms {
+
+namespace {
+
+constexpr int NV_THREADS = 512;
+constexpr int NV_WARPS = NV_THREADS / 32;
+
+__device__ __forceinline__ float4 mm_ld_reduce(const float4* p) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float mm_ld_reduce(const float* p) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mm_st(float4* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ float4 fma4(float s, float4 a, float4 b) {
+  return make_float4(__fmaf_rn(s, a.x, b.x), __fmaf_rn(s, a.y, b.y), __fmaf_rn(s, a.z, b.z),
+                     __fmaf_rn(s, a.w, b.w));
+}
+__device__ __forceinline__ float fma4(float s, float a, float b) { return __fmaf_rn(s, a, b); }
+
+}  // namespace
+
+struct NvlsKernelArgs {
+  ncclDevComm dev;
+  ncclWindow_t win;
+  const uint32_t* ihat;
+  const Sc3* sc3;
+  float* table;
+  const float* M;  // local view of this rank's M
+  int D;
+  float lr;
+  int rank, world;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a) {
+  constexpr int W = sizeof(T) / sizeof(float);
+  ncclCoopCta cta;
+  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
+                                         /*multimem=*/true);
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+
+  const int64_t Ug = a.sc3->u_global;
+  const int C = a.D / W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * NV_WARPS + warp;
+  const int64_t nw = (int64_t)gridDim.x * NV_WARPS;
+  T* mc = reinterpret_cast<T*>(ncclGetLsaMultimemPointer(a.win, 0, a.dev));
+  T* E = reinterpret_cast<T*>(a.table);
+  const T* Ml = reinterpret_cast<const T*>(a.M);
+
+  // owned slice: reduce through the switch, update, broadcast the new rows
+  {
+    const int64_t s0 = Ug * a.rank / a.world, s1 = Ug * (a.rank + 1) / a.world;
+    for (int64_t t = gw; s0 + t < s1; t += nw) {
+      const int64_t r = s0 + t;
+      T* er = E + (size_t)__ldg(a.ihat + r) * C;
+      T* mr = mc + (size_t)r * C;
+      int c = lane;
+      for (; c + 96 < C; c += 128) {
+        const T m0 = mm_ld_reduce(mr + c), m1 = mm_ld_reduce(mr + c + 32);
+        const T m2 = mm_ld_reduce(mr + c + 64), m3 = mm_ld_reduce(mr + c + 96);
+        const T e0 = fma4(-a.lr, m0, er[c]), e1 = fma4(-a.lr, m1, er[c + 32]);
+        const T e2 = fma4(-a.lr, m2, er[c + 64]), e3 = fma4(-a.lr, m3, er[c + 96]);
+        er[c] = e0;
+        er[c + 32] = e1;
+        er[c + 64] = e2;
+        er[c + 96] = e3;
+        mm_st(mr + c, e0);
+        mm_st(mr + c + 32, e1);
+        mm_st(mr + c + 64, e2);
+        mm_st(mr + c + 96, e3);
+      }
+      for (; c < C; c += 32) {
+        const T e = fma4(-a.lr, mm_ld_reduce(mr + c), er[c]);
+        er[c] = e;
+        mm_st(mr + c, e);
+      }
+    }
+  }
+  bar.sync(cta, cuda::memory_order_acq_rel);  // the other ranks' rows have landed
+
+  // rows owned by the other ranks: copy the broadcast result into E
+  for (int j = 0; j < a.world; ++j) {
+    if (j == a.rank) continue;
+    const int64_t s0 = Ug * j / a.world, s1 = Ug * (j + 1) / a.world;
+    for (int64_t t = gw; s0 + t < s1; t += nw) {
+      const int64_t r = s0 + t;
+      T* er = E + (size_t)__ldg(a.ihat + r) * C;
+      const T* mr = Ml + (size_t)r * C;
+      int c = lane;
+      for (; c + 96 < C; c += 128) {
+        const T v0 = __ldcg(mr + c), v1 = __ldcg(mr + c + 32);
+        const T v2 = __ldcg(mr + c + 64), v3 = __ldcg(mr + c + 96);
+        er[c] = v0;
+        er[c + 32] = v1;
+        er[c + 64] = v2;
+        er[c + 96] = v3;
+      }
+      for (; c < C; c += 32) er[c] = __ldcg(mr + c);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+struct NvlsState {
+  ncclWindow_t win = nullptr;
+  ncclDevComm dev{};
+  bool dev_ok = false;
+  int ctas = 0;
+};
+
+NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char* err,
+                       size_t errlen) {
+  NvlsState* st = new NvlsState();
+  st->ctas = num_sms < 128 ? num_sms : 128;
+  ncclResult_t r = ncclCommWindowRegister(comm, M, bytes, &st->win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    snprintf(err, errlen, "ncclCommWindowRegister: %s", ncclGetErrorString(r));
+    delete st;
+    return nullptr;
+  }
+  ncclDevCommRequirements req{};
+  req.lsaMultimem = true;
+  req.lsaBarrierCount = st->ctas;
+  r = ncclDevCommCreate(comm, &req, &st->dev);
+  if (r != ncclSuccess) {
+    snprintf(err, errlen, "ncclDevCommCreate(lsaMultimem): %s", ncclGetErrorString(r));
+    ncclCommWindowDeregister(comm, st->win);
+    delete st;
+    return nullptr;
+  }
+  if (!st->dev.lsaMultimem.mcBasePtr) {
+    snprintf(err, errlen, "no multimem (NVLS) mapping on this communicator");
+    ncclDevCommDestroy(comm, &st->dev);
+    ncclCommWindowDeregister(comm, st->win);
+    delete st;
+    return nullptr;
+  }
+  st->dev_ok = true;
+  return st;
+}
+
+void nvls_destroy(ncclComm_t comm, NvlsState* st) {
+  if (!st) return;
+  if (st->dev_ok) ncclDevCommDestroy(comm, &st->dev);
+  if (st->win) ncclCommWindowDeregister(comm, st->win);
+  delete st;
+}
+
+void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
+                        const float* M, int D, float lr, int rank, int world, cudaStream_t s) {
+  NvlsKernelArgs a;
+  a.dev = st->dev;
+  a.win = st->win;
+  a.ihat = ihat;
+  a.sc3 = sc3;
+  a.table = table;
+  a.M = M;
+  a.D = D;
+  a.lr = lr;
+  a.rank = rank;
+  a.world = world;
+  const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0;
+  if (v4)
+    k_nvls_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
+  else
+    k_nvls_update<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
+}
+
+}  // namespace lms

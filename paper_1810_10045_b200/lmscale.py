@@ -48,7 +48,8 @@ class StatsC(ctypes.Structure):
                 ("us_total", ctypes.c_double),
                 ("bytes_ids_gathered", _i64), ("bytes_grad_allreduce", _i64),
                 ("bytes_scatter", _i64), ("bytes_update", _i64), ("workspace_bytes", _i64),
-                ("kernels_last_call", _i32), ("kernels_total_lo", _i32)]
+                ("kernels_last_call", _i32), ("kernels_total_lo", _i32),
+                ("fused_s5_s6", _i32), ("nvls_available", _i32)]
 
 
 def _sig(name, res, args):

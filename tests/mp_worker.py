@@ -79,7 +79,47 @@ def run_small(ctx_full, cfg, mode, rank, G, dev):
     ctx.close()
 
 
-def run_full(cfg, rank, G, dev, n_rand=24):
+def run_fused_small(cfg, mode, rank, G, dev):
+    """lmscale_step (S1-S6 in one call; S5+S6 as the fused NVLS kernel when the
+    box has multicast) against the oracle; replicas must be bit-identical."""
+    lr = synth.default_lr(mode)
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    Dh = [synth.grad_values(cfg.K, cfg.D, mode, rank=g) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, mode)
+    ctx = make_context(cfg.V, cfg.K, cfg.D)
+    E = E0.to(dev)
+    ug = ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), E, lr,
+                  want_num_unique=True)
+    torch.cuda.synchronize()
+    st = ctx.stats()
+    if os.environ.get("LMSCALE_REQUIRE_NVLS") == "1":
+        assert st["fused_s5_s6"] == 1, "fused NVLS path did not run"
+    Eo = E0.numpy().copy()
+    ref = oracle.sync_unique(J, [d.numpy() for d in Dh], Eo, lr)
+    assert ug == ref["Ug"]
+    got = E.cpu().numpy()
+    if mode == "int":
+        np.testing.assert_array_equal(got, Eo)
+    else:
+        A = oracle.abs_scale(J, [d.numpy() for d in Dh], ref["Ihat"])
+        t = ref["Ihat"].astype(np.int64)
+        E0n = E0.numpy()
+        check_rows(got[t], E0n[t].astype(np.float64) - lr * ref["Mhat64"], np.abs(E0n[t]) + lr * A,
+                   "signed", f"fused G={G} {cfg.name}")
+        untouched = np.setdiff1d(np.arange(cfg.V), t)
+        np.testing.assert_array_equal(got[untouched], E0n[untouched])
+    check_replicas(E, f"fused {cfg.name} {mode}")
+    # a second step on the updated table: the fused kernel leaves M reusable
+    ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), E, lr)
+    torch.cuda.synchronize()
+    check_replicas(E, f"fused step 2 {cfg.name} {mode}")
+    if rank == 0:
+        print(f"fused={st['fused_s5_s6']} nvls={st['nvls_available']} G={G} {cfg.name} {mode}",
+              flush=True)
+    ctx.close()
+
+
+def run_full(cfg, rank, G, dev, n_rand=24, fused=False):
     """BASELINE full size on G real GPUs: integers in full, sampled float rows."""
     mode = "signed"
     lr = synth.default_lr(mode)
@@ -87,18 +127,24 @@ def run_full(cfg, rank, G, dev, n_rand=24):
     ctx = make_context(cfg.V, cfg.K, cfg.D)
     grad = synth.grad_values(cfg.K, cfg.D, mode, rank=rank, device=dev)
     E = synth.table_values(cfg.V, cfg.D, mode, device=dev)
-    sg = ctx.sync(torch.from_numpy(J[rank].view(np.int32)).to(dev), grad)
-    rows = sg.rows.clone()
-    ids = u32(sg.ids)
-    ctx.apply_update(E, sg, lr)
-    torch.cuda.synchronize()
     Ihat, gcounts = oracle.unique_global(np.concatenate(J))
+    if fused:
+        ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), grad, E, lr)
+        torch.cuda.synchronize()
+        ids = u32(ctx.sparse_grad().ids)
+        rows = None
+    else:
+        sg = ctx.sync(torch.from_numpy(J[rank].view(np.int32)).to(dev), grad)
+        rows = sg.rows.clone()
+        ids = u32(sg.ids)
+        ctx.apply_update(E, sg, lr)
+        torch.cuda.synchronize()
     np.testing.assert_array_equal(ids, Ihat)
     order = np.argsort(-gcounts, kind="stable")
     rng = np.random.default_rng(rank)
     words = np.unique(np.concatenate([Ihat[order[:6]], rng.choice(Ihat, n_rand, replace=False)]))
     slots = np.searchsorted(Ihat, words)
-    got = rows[torch.from_numpy(slots).to(dev)].cpu().numpy()
+    got = rows[torch.from_numpy(slots).to(dev)].cpu().numpy() if rows is not None else None
     gotE = E[torch.from_numpy(words.astype(np.int64)).to(dev)].cpu().numpy()
     E0 = synth.table_rows(cfg.V, cfg.D, mode, words).numpy().astype(np.float64)
     for i, w in enumerate(words):
@@ -108,7 +154,8 @@ def run_full(cfg, rank, G, dev, n_rand=24):
             Js.append(J[g][pos])
             Ds.append(synth.grad_rows(cfg.D, mode, pos, rank=g).numpy().reshape(len(pos), cfg.D))
         ref, A, n = oracle.type_gradient(Js, Ds, w)
-        check_rows(got[i:i + 1], ref[None], A[None], mode, f"{cfg.name} G={G} word {w}")
+        if got is not None:
+            check_rows(got[i:i + 1], ref[None], A[None], mode, f"{cfg.name} G={G} word {w}")
         check_rows(gotE[i:i + 1], (E0[i] - lr * ref)[None], (np.abs(E0[i]) + lr * A)[None],
                    "signed", f"{cfg.name} G={G} E row {w}")
     check_replicas(E, f"full {cfg.name}")
@@ -126,9 +173,13 @@ def main():
         for mode in ("int", "signed"):
             run_small(None, synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev)
         run_small(None, synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
+        for mode in ("int", "signed"):
+            run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev)
+        run_fused_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
     for name in ("1b", "char", "amazon", "tieba"):
         if name in which:
             run_full(synth.CONFIGS[name], rank, G, dev)
+            run_full(synth.CONFIGS[name], rank, G, dev, fused=True)
     dist.barrier()
     if rank == 0:
         print(f"MP_OK G={G} {which}", flush=True)
