@@ -118,6 +118,7 @@ NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char
                        size_t errlen);
 void nvls_destroy(ncclComm_t comm, NvlsState* st);
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
-                        const float* M, int D, float lr, int rank, int world, cudaStream_t s);
+                        const float* M, int D, float lr, int rank, int world,
+                        unsigned long long* trace, cudaStream_t s);
 
 }  // namespace lms

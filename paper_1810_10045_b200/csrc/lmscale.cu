@@ -593,9 +593,19 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   if (G > 1 && table && ctx->nvls) {
     // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
-                       ctx->cfg.rank, G, s);
+                       ctx->cfg.rank, G, ctx->trace, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
+    if (ctx->trace) {
+      cudaStreamSynchronize(s);
+      unsigned long long t[64];
+      cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
+      fprintf(stderr,
+              "[lmscale trace rank %d] nvls: barrier1 %.2f  reduce+update+bcast %.2f  barrier2 %.2f"
+              "  copy %.2f us | S3 start -> nvls start %.2f us\n",
+              ctx->cfg.rank, (t[49] - t[48]) * 1e-3, (t[50] - t[49]) * 1e-3,
+              (t[51] - t[50]) * 1e-3, (t[52] - t[51]) * 1e-3, (t[48] - t[32]) * 1e-3);
+    }
     rec(ctx, EV_UPD_BEGIN, s);
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);

@@ -21,6 +21,7 @@
 #include <nccl_device.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -71,15 +72,26 @@ struct NvlsKernelArgs {
   int D;
   float lr;
   int rank, world;
+  unsigned long long* trace;
 };
+
+__device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[i] = t;
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a) {
   constexpr int W = sizeof(T) / sizeof(float);
+  nv_stamp(a.trace, 48);
   ncclCoopCta cta;
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
                                          /*multimem=*/true);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  nv_stamp(a.trace, 49);
 
   const int64_t Ug = a.sc3->u_global;
   const int C = a.D / W;
@@ -119,7 +131,9 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
       }
     }
   }
+  nv_stamp(a.trace, 50);
   bar.sync(cta, cuda::memory_order_acq_rel);  // the other ranks' rows have landed
+  nv_stamp(a.trace, 51);
 
   // rows owned by the other ranks: copy the broadcast result into E
   for (int j = 0; j < a.world; ++j) {
@@ -141,6 +155,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
       for (; c < C; c += 32) er[c] = __ldcg(mr + c);
     }
   }
+  nv_stamp(a.trace, 52);
 }
 
 // ---------------------------------------------------------------- host side
@@ -156,6 +171,7 @@ NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char
                        size_t errlen) {
   NvlsState* st = new NvlsState();
   st->ctas = num_sms < 128 ? num_sms : 128;
+  if (const char* e = getenv("LMSCALE_NVLS_CTAS")) st->ctas = atoi(e);
   ncclResult_t r = ncclCommWindowRegister(comm, M, bytes, &st->win, NCCL_WIN_COLL_SYMMETRIC);
   if (r != ncclSuccess) {
     snprintf(err, errlen, "ncclCommWindowRegister: %s", ncclGetErrorString(r));
@@ -191,8 +207,10 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st) {
 }
 
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
-                        const float* M, int D, float lr, int rank, int world, cudaStream_t s) {
+                        const float* M, int D, float lr, int rank, int world,
+                        unsigned long long* trace, cudaStream_t s) {
   NvlsKernelArgs a;
+  a.trace = trace;
   a.dev = st->dev;
   a.win = st->win;
   a.ihat = ihat;

@@ -19,7 +19,21 @@ dev = torch.device("cuda", 0)
 ids = torch.from_numpy(synth.ids_for(cfg, 0).view(np.int32)).to(dev)
 grad = synth.grad_values(cfg.K, cfg.D, "signed", device=dev)
 table = synth.table_values(cfg.V, cfg.D, "signed", device=dev)
-ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+world = int(os.environ.get("WORLD_SIZE", "1"))
+if world > 1:
+    import torch.distributed as dist
+    from paper_1810_10045_b200.distributed import make_context
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank = dist.get_rank()
+    dev = torch.device("cuda", local)
+    ids = torch.from_numpy(synth.ids_for(cfg, rank).view(np.int32)).to(dev)
+    grad = synth.grad_values(cfg.K, cfg.D, "signed", rank=rank, device=dev)
+    table = synth.table_values(cfg.V, cfg.D, "signed", device=dev)
+    ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+else:
+    ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
 for i in range(steps):
     ctx.step(ids, grad, table, 0.1)
     torch.cuda.synchronize()
