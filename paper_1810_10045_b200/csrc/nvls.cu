@@ -110,19 +110,20 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
       T* er = E + (size_t)__ldg(a.ihat + r) * C;
       T* mr = mc + (size_t)r * C;
       int c = lane;
-      for (; c + 96 < C; c += 128) {
-        const T m0 = mm_ld_reduce(mr + c), m1 = mm_ld_reduce(mr + c + 32);
-        const T m2 = mm_ld_reduce(mr + c + 64), m3 = mm_ld_reduce(mr + c + 96);
-        const T e0 = fma4(-a.lr, m0, er[c]), e1 = fma4(-a.lr, m1, er[c + 32]);
-        const T e2 = fma4(-a.lr, m2, er[c + 64]), e3 = fma4(-a.lr, m3, er[c + 96]);
-        er[c] = e0;
-        er[c + 32] = e1;
-        er[c + 64] = e2;
-        er[c + 96] = e3;
-        mm_st(mr + c, e0);
-        mm_st(mr + c + 32, e1);
-        mm_st(mr + c + 64, e2);
-        mm_st(mr + c + 96, e3);
+      // 8 independent multicast reductions (+ 8 local E loads) in flight per lane
+      for (; c + 224 < C; c += 256) {
+        T m[8], e[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) m[q] = mm_ld_reduce(mr + c + 32 * q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) e[q] = er[c + 32 * q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          e[q] = fma4(-a.lr, m[q], e[q]);
+          er[c + 32 * q] = e[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mm_st(mr + c + 32 * q, e[q]);
       }
       for (; c < C; c += 32) {
         const T e = fma4(-a.lr, mm_ld_reduce(mr + c), er[c]);
