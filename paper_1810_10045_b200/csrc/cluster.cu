@@ -1,0 +1,255 @@
+// cluster.cu -- S1 (local unique, step 1) inside ONE thread-block
+// cluster for K <= 16 x 4096 tokens.
+//
+// The whole sort lives in distributed shared memory: CTA c of the cluster
+// owns sorted positions [4096c, 4096c + 4096).  Each LSD pass (<= 10-bit
+// digits) ranks the CTA's tile with warp multisplit (__match_any_sync),
+// publishes per-digit tile totals in its own shared memory, and after a
+// cluster barrier every CTA reads the other CTAs' totals over DSMEM to form its
+// bases and scatters its keys straight into the destination CTAs' shared
+// buffers.  No global round trips and no grid-wide barriers inside the sort:
+// cluster barriers cost a fraction of a grid sync.  The run flags / J^ /
+// inverse epilogue is the same as the cooperative kernel's.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lms {
+
+namespace {
+constexpr int CT = CL_THREADS;
+constexpr int NW = CL_THREADS / 32;
+constexpr int IT = CL_TILE / CL_THREADS;  // 8 keys per thread
+}  // namespace
+
+__global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
+  extern __shared__ uint32_t sm[];
+  __shared__ uint32_t s_scan[32];
+  __shared__ uint32_t s_heads;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank();
+  const int C = (int)cl.num_blocks();
+  const int ndig = 1 << a.bits;
+  uint32_t* kbuf[2] = {sm, sm + 2 * CL_TILE};
+  int32_t* vbuf[2] = {reinterpret_cast<int32_t*>(sm + CL_TILE),
+                      reinterpret_cast<int32_t*>(sm + 3 * CL_TILE)};
+  uint32_t* s_cnt = sm + 4 * CL_TILE;   // [NW][ndig]
+  uint32_t* s_tot = s_cnt + NW * ndig;  // [ndig] this tile's digit totals
+  uint32_t* s_base = s_tot + ndig;      // [ndig]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = a.K;
+  const int t0 = cr * CL_TILE;  // first global sorted position of this CTA
+
+  // zero the local presence bitmap (ordered before the epilogue by cluster barriers)
+  for (int64_t w = (int64_t)cr * CT + tid; w < a.W; w += (int64_t)C * CT) a.lbits[w] = 0u;
+  if (cr == 0 && tid == 0) {
+    a.sc->err = 0u;
+    a.sc->u_local = 0;
+    if (a.sc3) {
+      a.sc3->err = 0u;
+      a.sc3->u_global = 0;
+    }
+  }
+  bool bad = false;
+  int cur = 0;
+  for (int p = 0; p < a.passes; ++p) {
+    const int shift = p * a.bits;
+    const uint32_t mask = (uint32_t)(ndig - 1);
+    for (int i = tid; i < NW * ndig; i += CT) s_cnt[i] = 0;
+    uint32_t key[IT], rank[IT], dig[IT];
+    int32_t val[IT];
+    const int lb = warp * (32 * IT);  // local base of this warp (striped layout)
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int li = lb + j * 32 + lane;
+      const int gi = t0 + li;
+      if (gi < K) {
+        if (p == 0) {
+          key[j] = __ldcs(a.ids + gi);
+          val[j] = gi;
+          bad |= key[j] >= a.vocab;
+        } else {
+          key[j] = kbuf[cur][li];
+          val[j] = vbuf[cur][li];
+        }
+      } else {
+        key[j] = 0;
+        val[j] = -1;
+      }
+    }
+    __syncthreads();
+    uint32_t* wc = s_cnt + warp * ndig;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int gi = t0 + lb + j * 32 + lane;
+      const uint32_t d = gi < K ? ((key[j] >> shift) & mask) : 0xffffffffu;
+      dig[j] = d;
+      const unsigned m = __match_any_sync(FULL, d);
+      const uint32_t before = d != 0xffffffffu ? wc[d] : 0u;
+      rank[j] = before + __popc(m & lanemask_lt());
+      __syncwarp();
+      if (d != 0xffffffffu && lane == (__ffs(m) - 1)) wc[d] = before + __popc(m);
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int d = tid; d < ndig; d += CT) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t c = s_cnt[w * ndig + d];
+        s_cnt[w * ndig + d] = run;
+        run += c;
+      }
+      s_tot[d] = run;
+    }
+    cl.sync();  // every CTA's digit totals are published
+    const int dpt = ndig > CT ? ndig / CT : 1;
+    const int d0 = tid * dpt;
+    uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
+    if (d0 < ndig) {
+      for (int c = 0; c < C; ++c) {
+        const uint32_t* rt = cl.map_shared_rank(s_tot, c);
+        for (int k = 0; k < dpt; ++k) {
+          const uint32_t v = rt[d0 + k];
+          tot[k] += v;
+          if (c < cr) pre[k] += v;
+        }
+      }
+    }
+    uint32_t all;
+    uint32_t ex = block_excl_scan(tot[0] + tot[1] + tot[2] + tot[3], s_scan, &all);
+    if (d0 < ndig)
+      for (int k = 0; k < dpt; ++k) {
+        s_base[d0 + k] = ex + pre[k];
+        ex += tot[k];
+      }
+    __syncthreads();
+    // scatter into the destination CTAs' shared buffers
+    const int nxt = cur ^ 1;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const uint32_t d = dig[j];
+      if (d != 0xffffffffu) {
+        const uint32_t pos = s_base[d] + s_cnt[warp * ndig + d] + rank[j];
+        const int dst = (int)(pos / CL_TILE), off = (int)(pos % CL_TILE);
+        cl.map_shared_rank(kbuf[nxt], dst)[off] = key[j];
+        cl.map_shared_rank(vbuf[nxt], dst)[off] = val[j];
+      }
+    }
+    cl.sync();  // all keys landed; totals may be overwritten next pass
+    cur = nxt;
+  }
+  if (bad) {
+    atomicOr(&a.sc->err, 1u);
+    if (a.sc3) atomicOr(&a.sc3->err, 1u);
+  }
+
+  // ---- run flags over this CTA's sorted slice (blocked: 8 per thread)
+  const uint32_t* sk = kbuf[cur];
+  const int32_t* sv = vbuf[cur];
+  const int li0 = tid * IT;
+  uint32_t heads = 0;
+  uint32_t prev = 0;
+  if (li0 > 0)
+    prev = sk[li0 - 1];
+  else if (cr > 0)
+    prev = cl.map_shared_rank(sk, cr - 1)[CL_TILE - 1];
+#pragma unroll
+  for (int j = 0; j < IT; ++j) {
+    const int gi = t0 + li0 + j;
+    const bool h = gi < K && (gi == 0 || sk[li0 + j] != prev);
+    heads |= (uint32_t)h << j;
+    prev = sk[li0 + j];
+  }
+  uint32_t tile_heads;
+  const uint32_t excl_t = block_excl_scan(__popc(heads), s_scan, &tile_heads);
+  if (tid == 0) s_heads = tile_heads;
+  cl.sync();  // head counts published
+  uint32_t tile_excl = 0;
+  for (int c = 0; c < cr; ++c) tile_excl += *cl.map_shared_rank(&s_heads, c);
+  uint32_t u_run = tile_excl + excl_t;
+  bool bad2 = false;
+#pragma unroll
+  for (int j = 0; j < IT; ++j) {
+    const int li = li0 + j;
+    const int gi = t0 + li;
+    if (gi < K) {
+      const uint32_t key = sk[li];
+      const int32_t pos = sv[li];
+      a.va[gi] = pos;  // the stable permutation (sorted position -> token)
+      if ((heads >> j) & 1u) {
+        a.luniq[u_run] = key;
+        a.lstart[u_run] = gi;
+        if (a.ihat) {
+          a.ihat[u_run] = key;
+          a.l2g[u_run] = (int32_t)u_run;
+        }
+        if (key < a.vocab)
+          atomicOr(a.lbits + (key >> 5), 1u << (key & 31u));
+        else
+          bad2 = true;
+        ++u_run;
+      }
+      a.segidx[gi] = (int32_t)u_run - 1;
+      a.inverse[pos] = (int32_t)u_run - 1;
+      if (gi == K - 1) {
+        a.sc->u_local = u_run;
+        a.lstart[u_run] = K;
+        if (a.nu_out) *a.nu_out = u_run;
+        if (a.sc3) a.sc3->u_global = u_run;
+      }
+    }
+  }
+  if (bad2) {
+    atomicOr(&a.sc->err, 1u);
+    if (a.sc3) atomicOr(&a.sc3->err, 1u);
+  }
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+SortPlan make_cluster_plan(uint64_t vocab) {
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < vocab) ++bits;
+  SortPlan p;
+  p.passes = (bits + CL_MAX_BITS - 1) / CL_MAX_BITS;
+  p.bits = (bits + p.passes - 1) / p.passes;
+  return p;
+}
+
+size_t cluster_smem_bytes(int bits) {
+  return (size_t)(4 * CL_TILE + (NW + 2) * (1 << bits)) * 4;
+}
+
+bool cluster_s1_ok(int K) {
+  static int ok = -1;
+  if (ok < 0) {
+    ok = cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                 cudaSuccess &&
+         cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)cluster_smem_bytes(CL_MAX_BITS)) == cudaSuccess;
+    if (!ok) cudaGetLastError();
+  }
+  return ok && K >= 1 && K <= CL_MAX_CTAS * CL_TILE;
+}
+
+cudaError_t launch_s1_cluster(const S1Args& a, cudaStream_t s) {
+  const int C = (a.K + CL_TILE - 1) / CL_TILE;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(CL_THREADS);
+  cfg.dynamicSmemBytes = cluster_smem_bytes(a.bits);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_s1_cluster, a);
+}
+
+}  // namespace lms

@@ -125,6 +125,10 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
   if (blockIdx.x == 0 && tid == 0) {
     a.sc->err = 0u;
     a.sc->u_local = 0;
+    if (a.sc3) {
+      a.sc3->err = 0u;
+      a.sc3->u_global = 0;
+    }
   }
   bool bad = false;
 
@@ -207,7 +211,10 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
     kin = kout;
     vin = vout;
   }
-  if (bad) atomicOr(&a.sc->err, 1u);
+  if (bad) {
+    atomicOr(&a.sc->err, 1u);
+    if (a.sc3) atomicOr(&a.sc3->err, 1u);
+  }
 
   // ---- run-length flags over the sorted ids (blocked: 8 per thread)
   uint32_t heads = 0;
@@ -251,6 +258,10 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
         if ((heads >> j) & 1u) {
           a.luniq[u_run] = sk[j];
           a.lstart[u_run] = i;
+          if (a.ihat) {
+            a.ihat[u_run] = sk[j];
+            a.l2g[u_run] = (int32_t)u_run;
+          }
           if (sk[j] < a.vocab)
             atomicOr(a.lbits + (sk[j] >> 5), 1u << (sk[j] & 31u));
           else
@@ -263,10 +274,14 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
           a.sc->u_local = u_run;
           a.lstart[u_run] = K;
           if (a.nu_out) *a.nu_out = u_run;
+          if (a.sc3) a.sc3->u_global = u_run;
         }
       }
     }
-    if (bad2) atomicOr(&a.sc->err, 1u);
+    if (bad2) {
+      atomicOr(&a.sc->err, 1u);
+      if (a.sc3) atomicOr(&a.sc3->err, 1u);
+    }
     __syncthreads();
   }
   stamp(a.trace, 22);

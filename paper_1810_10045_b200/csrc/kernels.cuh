@@ -56,6 +56,11 @@ struct S1Args {
   Sc1* sc;
   int64_t* nu_out;
   unsigned long long* trace;  // optional phase timestamps (LMSCALE_PHASE_TRACE)
+  // world == 1 shortcut (I = J, so I^ = J^, U_g = U_i, l2g = identity): when
+  // non-null, S1 also writes I^, l2g and the S3 scalars and S3 is skipped.
+  uint32_t* ihat;
+  int32_t* l2g;
+  Sc3* sc3;
 };
 struct S3Args {
   const uint32_t* I;
@@ -73,6 +78,17 @@ struct S3Args {
   unsigned long long* trace;
 };
 SortPlan make_coop_plan(uint64_t vocab);
+
+// ---- cluster S1 (cluster.cu): K <= CL_MAX_CTAS * CL_TILE, one cluster ------
+constexpr int CL_THREADS = 512;
+constexpr int CL_TILE = 4096;
+constexpr int CL_MAX_BITS = 10;
+constexpr int CL_MAX_CTAS = 16;
+SortPlan make_cluster_plan(uint64_t vocab);
+size_t cluster_smem_bytes(int bits);
+bool cluster_s1_ok(int K);
+// Writes the stable permutation to a.va (a.ka/a.kb/a.vb unused).
+cudaError_t launch_s1_cluster(const S1Args& a, cudaStream_t s);
 size_t s1_smem_bytes(int bits);
 cudaError_t launch_s1(const S1Args& a, int num_sms, cudaStream_t s);
 cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s);

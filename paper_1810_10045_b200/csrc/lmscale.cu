@@ -48,7 +48,7 @@ struct lmscale_ctx {
   lmscale_config cfg;
   int num_sms = 0;
   int64_t K = 0, W = 0, NI = 0, ucap = 0, nchunks = 0, ntiles_max = 0, ntp_max = 0;
-  SortPlan plan{};
+  SortPlan plan{}, cl_plan{};
   cudaStream_t s_side = nullptr, s_copy = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_s1 = nullptr, ev_s3 = nullptr, ev_copy = nullptr;
   cudaEvent_t tev[EV_COUNT] = {};
@@ -151,8 +151,11 @@ void end_call(lmscale_ctx* c) {
 
 // S1 on stream s: one cooperative launch (radix sort + run flags).
 lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t* nu_out,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool world1 = false) {
   S1Args a;
+  a.ihat = world1 ? ctx->ihat : nullptr;
+  a.l2g = world1 ? ctx->l2g : nullptr;
+  a.sc3 = world1 ? ctx->sc3 : nullptr;
   a.ids = ids;
   a.K = (int)k;
   a.vocab = (uint32_t)ctx->cfg.vocab;
@@ -175,13 +178,24 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   a.sc = ctx->sc1;
   a.nu_out = nu_out;
   a.trace = ctx->trace;
-  CK(launch_s1(a, ctx->num_sms, s));
-  LAUNCHED(1);
-  ctx->sorted_keys = (a.passes & 1) ? ctx->keys_a : ctx->keys_b;
-  ctx->sorted_vals = (a.passes & 1) ? ctx->vals_a : ctx->vals_b;
+  if (!getenv("LMSCALE_NO_CLUSTER") && cluster_s1_ok((int)k)) {
+    // small K: the whole sort in one thread-block cluster (DSMEM)
+    a.passes = ctx->cl_plan.passes;
+    a.bits = ctx->cl_plan.bits;
+    CK(launch_s1_cluster(a, s));
+    LAUNCHED(1);
+    ctx->sorted_keys = nullptr;
+    ctx->sorted_vals = ctx->vals_a;
+  } else {
+    CK(launch_s1(a, ctx->num_sms, s));
+    LAUNCHED(1);
+    ctx->sorted_keys = (a.passes & 1) ? ctx->keys_a : ctx->keys_b;
+    ctx->sorted_vals = (a.passes & 1) ? ctx->vals_a : ctx->vals_b;
+  }
   ctx->last_k = k;
   ctx->have_s1 = true;
-  ctx->have_s3 = false;
+  ctx->have_s3 = world1;
+  if (world1) ctx->last_n = k;
   return LMSCALE_OK;
 }
 
@@ -307,6 +321,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->ntiles_max = (ctx->K + CO_TILE - 1) / CO_TILE;
     ctx->ntp_max = (ctx->ntiles_max + 3) / 4 * 4;
     ctx->plan = make_coop_plan((uint64_t)cfg->vocab);
+    ctx->cl_plan = make_cluster_plan((uint64_t)cfg->vocab);
     const int64_t K = ctx->K, D = cfg->dim;
     // ---- workspace layout (one allocation, 256-byte aligned sub-buffers)
     size_t off = 0;
@@ -570,16 +585,19 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     rec(ctx, EV_GATHER_END, s);
     CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
   } else {
+    // world 1: I = J, so S3's I^, U_g and l2g come out of S1 (one launch).
     rec(ctx, EV_S1_BEGIN, s);
-    st = run_s1(ctx, ids, k, nullptr, s);
+    st = run_s1(ctx, ids, k, nullptr, s, /*world1=*/true);
     if (st) return st;
     rec(ctx, EV_S1_END, s);
     rec(ctx, EV_GATHER_END, s);
   }
   rec(ctx, EV_JOIN, s);
   // S3: I^, U_g, l2g; {U_g, err, U_i} to the host on the copy stream.
-  st = run_s3(ctx, I, n, s);
-  if (st) return st;
+  if (G > 1) {
+    st = run_s3(ctx, I, n, s);
+    if (st) return st;
+  }
   rec(ctx, EV_S3_END, s);
   CK(cudaEventRecord(ctx->ev_s3, s));
   CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_s3, 0));

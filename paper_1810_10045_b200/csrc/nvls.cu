@@ -3,8 +3,7 @@
 // P:421) in ONE kernel, through NCCL 2.28's device API.
 //
 // M (U_g x D, one copy per rank) sits in an NCCL symmetric window with a
-// multicast (multimem) mapping on the NVSwitch.  Rank i owns the slice of rows
-// [U_g*i/G, U_g*(i+1)/G):
+// multicast (multimem) mapping on the NVSwitch.  Rank i owns rows r = i mod G:
 //   1. LSA barrier: every rank's M_g is complete (S4 ran before on each rank);
 //   2. for each owned row: multimem.ld_reduce (the switch sums the G copies),
 //      e' = fma(-lr, m, E[I^[r]]) written to the local E, and multimem.st of e'
@@ -73,6 +72,7 @@ struct NvlsKernelArgs {
   float lr;
   int rank, world;
   unsigned long long* trace;
+  int diag;  // timing diagnostics only (LMSCALE_NVLS_DIAG): 1 no broadcast, 2 no reduce
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -102,19 +102,25 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
   T* E = reinterpret_cast<T*>(a.table);
   const T* Ml = reinterpret_cast<const T*>(a.M);
 
-  // owned slice: reduce through the switch, update, broadcast the new rows
+  // owned rows r = rank + G*t (interleaved over the id space, so every rank
+  // gets the same mix of hot and cold rows): reduce through the switch,
+  // update, broadcast the new rows
   {
-    const int64_t s0 = Ug * a.rank / a.world, s1 = Ug * (a.rank + 1) / a.world;
-    for (int64_t t = gw; s0 + t < s1; t += nw) {
-      const int64_t r = s0 + t;
+    for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
+      const int64_t r = a.rank + a.world * t;
       T* er = E + (size_t)__ldg(a.ihat + r) * C;
       T* mr = mc + (size_t)r * C;
       int c = lane;
       // 8 independent multicast reductions (+ 8 local E loads) in flight per lane
       for (; c + 224 < C; c += 256) {
         T m[8], e[8];
+        if (a.diag == 2) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) m[q] = mm_ld_reduce(mr + c + 32 * q);
+          for (int q = 0; q < 8; ++q) m[q] = __ldcg(reinterpret_cast<const T*>(a.M) + (mr - mc) + c + 32 * q);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) m[q] = mm_ld_reduce(mr + c + 32 * q);
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) e[q] = er[c + 32 * q];
 #pragma unroll
@@ -122,8 +128,10 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
           e[q] = fma4(-a.lr, m[q], e[q]);
           er[c + 32 * q] = e[q];
         }
+        if (a.diag != 1) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mm_st(mr + c + 32 * q, e[q]);
+          for (int q = 0; q < 8; ++q) mm_st(mr + c + 32 * q, e[q]);
+        }
       }
       for (; c < C; c += 32) {
         const T e = fma4(-a.lr, mm_ld_reduce(mr + c), er[c]);
@@ -139,9 +147,8 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
   // rows owned by the other ranks: copy the broadcast result into E
   for (int j = 0; j < a.world; ++j) {
     if (j == a.rank) continue;
-    const int64_t s0 = Ug * j / a.world, s1 = Ug * (j + 1) / a.world;
-    for (int64_t t = gw; s0 + t < s1; t += nw) {
-      const int64_t r = s0 + t;
+    for (int64_t t = gw; j + a.world * t < Ug; t += nw) {
+      const int64_t r = j + a.world * t;
       T* er = E + (size_t)__ldg(a.ihat + r) * C;
       const T* mr = Ml + (size_t)r * C;
       int c = lane;
@@ -212,6 +219,8 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
                         unsigned long long* trace, cudaStream_t s) {
   NvlsKernelArgs a;
   a.trace = trace;
+  static const int diag = getenv("LMSCALE_NVLS_DIAG") ? atoi(getenv("LMSCALE_NVLS_DIAG")) : 0;
+  a.diag = diag;
   a.dev = st->dev;
   a.win = st->win;
   a.ihat = ihat;

@@ -66,6 +66,14 @@ def test_unique_edge_cases(lm, name, V, J):
     ctx.close()
 
 
+@pytest.mark.parametrize("name,V,J", UNIQUE_CASES[:5] + UNIQUE_CASES[6:],
+                         ids=[c[0] for c in UNIQUE_CASES[:5] + UNIQUE_CASES[6:]])
+def test_unique_cooperative_path_small_k(lm, name, V, J, monkeypatch):
+    """Small K normally takes the one-cluster S1; force the cooperative one."""
+    monkeypatch.setenv("LMSCALE_NO_CLUSTER", "1")
+    test_unique_edge_cases(lm, name, V, J)
+
+
 @pytest.mark.parametrize("name", list(synth.CONFIGS))
 def test_unique_every_config(lm, name):
     cfg = synth.CONFIGS[name]
