@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches (no CUDA graph)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
@@ -172,7 +173,8 @@ def run_reference(args, cfg, rank, world):
 def config_dict(cfg, args, world):
     return {"workload": cfg.name, "V": cfg.V, "K_per_gpu": cfg.K, "D": cfg.D, "zipf_s": cfg.s,
             "G": world, "value_mode": args.mode, "global_tokens": world * cfg.K,
-            "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)"}
+            "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)",
+            "cuda_graph": not getattr(args, "no_graph", True)}
 
 
 def emit(line, args):
@@ -220,10 +222,11 @@ def main():
     lr = synth.default_lr(args.mode)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
+    flags = lmscale.FLAG_TIMING | (0 if args.no_graph else lmscale.FLAG_GRAPH)
     if world > 1:
-        ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+        ctx = make_context(cfg.V, cfg.K, cfg.D, flags=flags)
     else:
-        ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, device=local, flags=lmscale.FLAG_TIMING)
+        ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, device=local, flags=flags)
     stream = torch.cuda.current_stream()
 
     def barrier():

@@ -6,5 +6,5 @@ Importing the binding raises if the library has not been built -- there is
 no CPU fallback.
 """
 from .lmscale import (Context, LmscaleError, SparseGrad, get_nccl_id, version,  # noqa: F401
-                      FLAG_NO_COMM, FLAG_TIMING, LIB_PATH)
+                      FLAG_NO_COMM, FLAG_TIMING, FLAG_GRAPH, LIB_PATH)
 from . import distributed  # noqa: F401

@@ -20,6 +20,13 @@ namespace cg = cooperative_groups;
 namespace lms {
 
 namespace {
+__device__ __forceinline__ void cstamp(unsigned long long* tr, int i) {
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[i] = t;
+  }
+}
 constexpr int CT = CL_THREADS;
 constexpr int NW = CL_THREADS / 32;
 constexpr int IT = CL_TILE / CL_THREADS;  // 8 keys per thread
@@ -33,9 +40,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   const int cr = (int)cl.block_rank();
   const int C = (int)cl.num_blocks();
   const int ndig = 1 << a.bits;
-  uint32_t* kbuf[2] = {sm, sm + 2 * CL_TILE};
-  int32_t* vbuf[2] = {reinterpret_cast<int32_t*>(sm + CL_TILE),
-                      reinterpret_cast<int32_t*>(sm + 3 * CL_TILE)};
+  // (key, val) pairs, ping-pong: one 8-byte DSMEM store per element
+  uint2* kv[2] = {reinterpret_cast<uint2*>(sm), reinterpret_cast<uint2*>(sm + 2 * CL_TILE)};
   uint32_t* s_cnt = sm + 4 * CL_TILE;   // [NW][ndig]
   uint32_t* s_tot = s_cnt + NW * ndig;  // [ndig] this tile's digit totals
   uint32_t* s_base = s_tot + ndig;      // [ndig]
@@ -43,6 +49,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   const int K = a.K;
   const int t0 = cr * CL_TILE;  // first global sorted position of this CTA
 
+  cstamp(a.trace, 0);
   // zero the local presence bitmap (ordered before the epilogue by cluster barriers)
   for (int64_t w = (int64_t)cr * CT + tid; w < a.W; w += (int64_t)C * CT) a.lbits[w] = 0u;
   if (cr == 0 && tid == 0) {
@@ -72,8 +79,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
           val[j] = gi;
           bad |= key[j] >= a.vocab;
         } else {
-          key[j] = kbuf[cur][li];
-          val[j] = vbuf[cur][li];
+          const uint2 e = kv[cur][li];
+          key[j] = e.x;
+          val[j] = (int32_t)e.y;
         }
       } else {
         key[j] = 0;
@@ -105,17 +113,36 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
       }
       s_tot[d] = run;
     }
+    cstamp(a.trace, 1 + 4 * p);
     cl.sync();  // every CTA's digit totals are published
+    cstamp(a.trace, 2 + 4 * p);
     const int dpt = ndig > CT ? ndig / CT : 1;
     const int d0 = tid * dpt;
     uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
     if (d0 < ndig) {
-      for (int c = 0; c < C; ++c) {
-        const uint32_t* rt = cl.map_shared_rank(s_tot, c);
-        for (int k = 0; k < dpt; ++k) {
-          const uint32_t v = rt[d0 + k];
-          tot[k] += v;
-          if (c < cr) pre[k] += v;
+      if (dpt == 2) {
+        uint2 v[CL_MAX_CTAS];
+#pragma unroll
+        for (int c = 0; c < CL_MAX_CTAS; ++c)
+          if (c < C) v[c] = *reinterpret_cast<const uint2*>(cl.map_shared_rank(s_tot, c) + d0);
+#pragma unroll
+        for (int c = 0; c < CL_MAX_CTAS; ++c)
+          if (c < C) {
+            tot[0] += v[c].x;
+            tot[1] += v[c].y;
+            if (c < cr) {
+              pre[0] += v[c].x;
+              pre[1] += v[c].y;
+            }
+          }
+      } else {
+        for (int c = 0; c < C; ++c) {
+          const uint32_t* rt = cl.map_shared_rank(s_tot, c);
+          for (int k = 0; k < dpt; ++k) {
+            const uint32_t v = rt[d0 + k];
+            tot[k] += v;
+            if (c < cr) pre[k] += v;
+          }
         }
       }
     }
@@ -127,6 +154,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
         ex += tot[k];
       }
     __syncthreads();
+    cstamp(a.trace, 3 + 4 * p);
     // scatter into the destination CTAs' shared buffers
     const int nxt = cur ^ 1;
 #pragma unroll
@@ -135,11 +163,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
       if (d != 0xffffffffu) {
         const uint32_t pos = s_base[d] + s_cnt[warp * ndig + d] + rank[j];
         const int dst = (int)(pos / CL_TILE), off = (int)(pos % CL_TILE);
-        cl.map_shared_rank(kbuf[nxt], dst)[off] = key[j];
-        cl.map_shared_rank(vbuf[nxt], dst)[off] = val[j];
+        cl.map_shared_rank(kv[nxt], dst)[off] = make_uint2(key[j], (uint32_t)val[j]);
       }
     }
     cl.sync();  // all keys landed; totals may be overwritten next pass
+    cstamp(a.trace, 4 + 4 * p);
     cur = nxt;
   }
   if (bad) {
@@ -148,26 +176,32 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   }
 
   // ---- run flags over this CTA's sorted slice (blocked: 8 per thread)
-  const uint32_t* sk = kbuf[cur];
-  const int32_t* sv = vbuf[cur];
+  const uint2* skv = kv[cur];
   const int li0 = tid * IT;
   uint32_t heads = 0;
   uint32_t prev = 0;
   if (li0 > 0)
-    prev = sk[li0 - 1];
+    prev = skv[li0 - 1].x;
   else if (cr > 0)
-    prev = cl.map_shared_rank(sk, cr - 1)[CL_TILE - 1];
+    prev = cl.map_shared_rank(skv, cr - 1)[CL_TILE - 1].x;
+  uint32_t sk[IT];
+  int32_t sv[IT];
 #pragma unroll
   for (int j = 0; j < IT; ++j) {
+    const uint2 e = skv[li0 + j];
+    sk[j] = e.x;
+    sv[j] = (int32_t)e.y;
     const int gi = t0 + li0 + j;
-    const bool h = gi < K && (gi == 0 || sk[li0 + j] != prev);
+    const bool h = gi < K && (gi == 0 || sk[j] != prev);
     heads |= (uint32_t)h << j;
-    prev = sk[li0 + j];
+    prev = sk[j];
   }
   uint32_t tile_heads;
   const uint32_t excl_t = block_excl_scan(__popc(heads), s_scan, &tile_heads);
   if (tid == 0) s_heads = tile_heads;
+  cstamp(a.trace, 20);
   cl.sync();  // head counts published
+  cstamp(a.trace, 21);
   uint32_t tile_excl = 0;
   for (int c = 0; c < cr; ++c) tile_excl += *cl.map_shared_rank(&s_heads, c);
   uint32_t u_run = tile_excl + excl_t;
@@ -177,8 +211,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
     const int li = li0 + j;
     const int gi = t0 + li;
     if (gi < K) {
-      const uint32_t key = sk[li];
-      const int32_t pos = sv[li];
+      const uint32_t key = sk[j];
+      const int32_t pos = sv[j];
       a.va[gi] = pos;  // the stable permutation (sorted position -> token)
       if ((heads >> j) & 1u) {
         a.luniq[u_run] = key;
@@ -207,6 +241,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
     atomicOr(&a.sc->err, 1u);
     if (a.sc3) atomicOr(&a.sc3->err, 1u);
   }
+  cstamp(a.trace, 22);
   cl.sync();  // no CTA leaves while another may still read its shared memory
 }
 
@@ -229,7 +264,9 @@ bool cluster_s1_ok(int K) {
     ok = cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                  cudaSuccess &&
          cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)cluster_smem_bytes(CL_MAX_BITS)) == cudaSuccess;
+                              (int)cluster_smem_bytes(CL_MAX_BITS)) == cudaSuccess &&
+         cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              100) == cudaSuccess;
     if (!ok) cudaGetLastError();
   }
   return ok && K >= 1 && K <= CL_MAX_CTAS * CL_TILE;

@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 namespace lms {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -103,6 +105,13 @@ __device__ __forceinline__ uint32_t lookback_one(uint32_t* state, uint32_t tile,
   }
   st_release(state + tile, LB_INC | (excl + agg));
   return excl;
+}
+
+// One carveout for every kernel of the library (max shared memory): the SMs
+// are then never reconfigured between the step's kernels.
+inline void max_carveout(const void* f) {
+  static const bool off = getenv("LMSCALE_NO_CARVEOUT") != nullptr;
+  if (!off) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 }  // namespace lms

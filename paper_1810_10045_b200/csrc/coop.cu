@@ -452,6 +452,7 @@ int coop_grid_s1(int ntiles, int num_sms) {
   if (occ < 0) {
     cudaFuncSetAttribute(k_s1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)s1_smem_bytes(CO_MAX_BITS));
+    max_carveout((const void*)k_s1);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_s1, CO_THREADS,
                                                       s1_smem_bytes(CO_MAX_BITS)) != cudaSuccess ||
         occ < 1)
@@ -471,6 +472,7 @@ cudaError_t launch_s1(const S1Args& a, int num_sms, cudaStream_t s) {
 cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s) {
   static int occ = -1;
   if (occ < 0) {
+    max_carveout((const void*)k_s3);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_s3, CO_THREADS, 0) != cudaSuccess ||
         occ < 1)
       occ = 1;

@@ -82,6 +82,18 @@ struct lmscale_ctx {
   int64_t last_ug = 0;
   bool have_pending_ug = false;  // last step did not read U_g back to the host
   bool fused_last = false;       // last step used the fused NVLS S5+S6 kernel
+  // CUDA graph of lmscale_step (LMSCALE_FLAG_GRAPH)
+  bool capturing = false;
+  cudaStream_t s_cap = nullptr;
+  cudaEvent_t ev_cap = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  struct {
+    const void *ids, *grad, *table;
+    int64_t k;
+    float lr;
+    int kernels;
+    bool fused;
+  } gkey{};
   lmscale_stats stats{};
   int kernels_call = 0;
   int64_t kernels_total = 0;
@@ -136,7 +148,11 @@ bool comm_enabled(const lmscale_ctx* c) {
 bool timing(const lmscale_ctx* c) { return (c->cfg.flags & LMSCALE_FLAG_TIMING) != 0; }
 
 void rec(lmscale_ctx* c, int ev, cudaStream_t s) {
-  if (timing(c)) cudaEventRecord(c->tev[ev], s);
+  if (!timing(c)) return;
+  if (c->capturing)  // a timing node inside the CUDA graph
+    cudaEventRecordWithFlags(c->tev[ev], s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(c->tev[ev], s);
 }
 
 void begin_call(lmscale_ctx* c) {
@@ -221,6 +237,21 @@ lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream
   ctx->last_n = n;
   ctx->have_s3 = true;
   return LMSCALE_OK;
+}
+
+void print_trace(lmscale_ctx* ctx, cudaStream_t s) {
+  if (!ctx->trace || ctx->capturing) return;
+  cudaStreamSynchronize(s);
+  unsigned long long t[64];
+  cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
+  fprintf(stderr, "[lmscale trace] S1:");
+  for (int i = 1; i <= 22; ++i)
+    if (t[i] && t[i - 1]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[0]) * 1e-3);
+  fprintf(stderr, " | S3:");
+  for (int i = 33; i <= 41; ++i)
+    if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
+  if (t[32] > t[0]) fprintf(stderr, " | S1start->S3start %.2f us", (t[32] - t[0]) * 1e-3);
+  fprintf(stderr, "\n");
 }
 
 ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
@@ -379,6 +410,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     CK(cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_s3, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&ctx->s_cap, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
     if (timing(ctx))
       for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&ctx->tev[i]));
     if (comm_enabled(ctx)) {
@@ -449,6 +482,9 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   if (ctx->s_side) cudaStreamDestroy(ctx->s_side);
   if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->s_cap) cudaStreamDestroy(ctx->s_cap);
+  if (ctx->ev_cap) cudaEventDestroy(ctx->ev_cap);
   if (ctx->h_sc3) cudaFreeHost(ctx->h_sc3);
   if (ctx->base) cudaFree(ctx->base);
   if (ctx->trace) cudaFree(ctx->trace);
@@ -599,11 +635,16 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     if (st) return st;
   }
   rec(ctx, EV_S3_END, s);
-  CK(cudaEventRecord(ctx->ev_s3, s));
-  CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_s3, 0));
-  CK(cudaMemcpyAsync(ctx->h_sc3, ctx->sc3, sizeof(Sc3) + sizeof(Sc1), cudaMemcpyDeviceToHost,
-                     ctx->s_copy));
-  CK(cudaEventRecord(ctx->ev_copy, ctx->s_copy));
+  // The host reads {U_g, err, U_i} only when it must: for NCCL's element count
+  // (G > 1 without the fused NVLS kernel) or when the caller asks for U_g.
+  const bool host_reads = need_host_ug || !(table && (G == 1 || ctx->nvls));
+  if (host_reads) {
+    CK(cudaEventRecord(ctx->ev_s3, s));
+    CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_s3, 0));
+    CK(cudaMemcpyAsync(ctx->h_sc3, ctx->sc3, sizeof(Sc3) + sizeof(Sc1), cudaMemcpyDeviceToHost,
+                       ctx->s_copy));
+    CK(cudaEventRecord(ctx->ev_copy, ctx->s_copy));
+  }
   // S4: segmented scatter-add into M.
   st = run_s4(ctx, grad, s);
   if (st) return st;
@@ -614,7 +655,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
                        ctx->cfg.rank, G, ctx->trace, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
-    if (ctx->trace) {
+    if (ctx->trace && !ctx->capturing) {
       cudaStreamSynchronize(s);
       unsigned long long t[64];
       cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
@@ -661,6 +702,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
     ctx->have_pending_ug = true;
+    print_trace(ctx, s);
     if (out) {
       out->ids = ctx->ihat;
       out->rows = ctx->M;
@@ -692,18 +734,8 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
   }
-  if (ctx->trace) {
-    cudaStreamSynchronize(s);
-    unsigned long long t[64];
-    cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[lmscale trace] S1:");
-    for (int i = 1; i <= 22; ++i)
-      if (t[i] && t[i - 1]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[0]) * 1e-3);
-    fprintf(stderr, " | S3:");
-    for (int i = 33; i <= 41; ++i)
-      if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
-    fprintf(stderr, " | S1start->S3start %.2f us\n", (t[32] - t[0]) * 1e-3);
-  }
+  print_trace(ctx, s);
+
   if (out) {
     out->ids = ctx->ihat;
     out->rows = ctx->M;
@@ -732,6 +764,62 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
 lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* grad, int64_t k,
                             float* table, float lr, int64_t* num_unique_out, void* stream) {
   if (ctx && !table) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "table is NULL");
+  // CUDA-graph replay: the step has no host round trip when world == 1 or the
+  // fused NVLS kernel is available, so it is captured once per argument tuple
+  // and replayed (one launch instead of ~5 kernels + events + NCCL calls).
+  if (ctx && (ctx->cfg.flags & LMSCALE_FLAG_GRAPH) && !num_unique_out &&
+      (ctx->cfg.world == 1 || ctx->nvls)) {
+    lmscale_status st0 = check_ids_args(ctx, ids, k);
+    if (st0) return st0;
+    cudaStream_t s = S(stream);
+    const bool hit = ctx->gexec && ctx->gkey.ids == ids && ctx->gkey.grad == grad &&
+                     ctx->gkey.table == table && ctx->gkey.k == k && ctx->gkey.lr == lr;
+    if (!hit) {
+      if (ctx->gexec) {
+        cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+      }
+      // capture on the library's own stream (the caller's may be the legacy
+      // default stream, which cannot be captured)
+      CK(cudaStreamBeginCapture(ctx->s_cap, cudaStreamCaptureModeThreadLocal));
+      ctx->capturing = true;
+      lmscale_sparse_grad sg;
+      lmscale_status st = step_impl(ctx, ids, grad, k, table, lr, false, &sg, ctx->s_cap);
+      ctx->capturing = false;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(ctx->s_cap, &g);
+      if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      if (e != cudaSuccess)
+        return fail(ctx, LMSCALE_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&ctx->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        ctx->gexec = nullptr;
+        return fail(ctx, LMSCALE_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+      }
+      ctx->gkey.ids = ids;
+      ctx->gkey.grad = grad;
+      ctx->gkey.table = table;
+      ctx->gkey.k = k;
+      ctx->gkey.lr = lr;
+      ctx->gkey.kernels = ctx->kernels_call;
+      ctx->gkey.fused = ctx->fused_last;
+      ctx->kernels_total -= ctx->kernels_call;  // captured, not launched yet
+    }
+    begin_call(ctx);
+    CK(cudaGraphLaunch(ctx->gexec, s));
+    ctx->kernels_call = ctx->gkey.kernels;
+    ctx->fused_last = ctx->gkey.fused;
+    ctx->timing_valid = timing(ctx);
+    ctx->update_timed = timing(ctx);
+    ctx->have_s1 = ctx->have_s3 = true;
+    ctx->last_k = k;
+    end_call(ctx);
+    return LMSCALE_OK;
+  }
   lmscale_sparse_grad sg;
   lmscale_status st =
       step_impl(ctx, ids, grad, k, table, lr, num_unique_out != nullptr, &sg, stream);

@@ -232,6 +232,9 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
   a.rank = rank;
   a.world = world;
   const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0;
+  static bool once = (max_carveout((const void*)k_nvls_update<float4>),
+                      max_carveout((const void*)k_nvls_update<float>), true);
+  (void)once;
   if (v4)
     k_nvls_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
   else

@@ -270,6 +270,7 @@ static void scatter_t(const ScatterArgs& a, cudaStream_t s) {
   int64_t blocks = (warps * 32 + SC_THREADS - 1) / SC_THREADS;
   static int occ = 0;  // resident CTAs per SM for this instantiation (persistent grid)
   if (!occ) {
+    max_carveout((const void*)k_scatter<T, NV, UNR>);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<T, NV, UNR>, SC_THREADS,
                                                       0) != cudaSuccess || occ < 1)
       occ = 1;
@@ -289,6 +290,8 @@ static void fixup_t(const ScatterArgs& a, cudaStream_t s) {
   const int64_t cap = (int64_t)a.num_sms * 4;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  static bool once = (max_carveout((const void*)k_fixup<T, NV>), true);
+  (void)once;
   k_fixup<T, NV><<<(unsigned)blocks, FX_THREADS, 0, s>>>(a);
 }
 
@@ -360,6 +363,9 @@ void launch_update(float* table, int D, const uint32_t* ids, const float* rows, 
   const int64_t cap = (int64_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)rows % 16 == 0;
+  static bool once = (max_carveout((const void*)k_update<float4>),
+                      max_carveout((const void*)k_update<float>), true);
+  (void)once;
   if (v4)
     k_update<float4><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, rows, n, n_dev, lr);
   else

@@ -25,6 +25,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK, INVALID_ARG, ID_RANGE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED = range(7)
 FLAG_NO_COMM = 1
 FLAG_TIMING = 2
+FLAG_GRAPH = 4
 
 _P = ctypes.c_void_p
 _i64 = ctypes.c_int64

@@ -193,6 +193,36 @@ def test_world1_collective_equals_oracle(lm):
         ctx.close()
 
 
+def test_graph_replay_equals_eager(lm):
+    """LMSCALE_FLAG_GRAPH: captured once, replayed; new values in the same
+    buffers are picked up, new buffers trigger a re-capture."""
+    cfg = synth.CONFIGS["tiny"].with_(G=1)
+    J, Dl, E0 = _inputs(cfg, 1, "signed")
+    J2, Dl2, _ = _inputs(cfg, 1, "signed", step=1)
+    eager = lm.Context(cfg.V, cfg.K, cfg.D)
+    graph = lm.Context(cfg.V, cfg.K, cfg.D, flags=lm.FLAG_GRAPH | lm.FLAG_TIMING)
+    ids, g = to_dev_ids(J[0]), Dl[0].to(dev())
+    Ea, Eb = E0.to(dev()), E0.to(dev())
+    for step in range(3):
+        if step == 2:   # same buffers, new contents
+            ids.copy_(to_dev_ids(J2[0]))
+            g.copy_(Dl2[0].to(dev()))
+        eager.step(ids, g, Ea, 0.1)
+        graph.step(ids, g, Eb, 0.1)
+        torch.cuda.synchronize()
+        assert torch.equal(Ea, Eb), step
+    st = graph.stats()
+    assert st["us_scatter"] > 0 and st["kernels_last_call"] >= 3
+    # different buffers: re-capture
+    ids3, g3, Ec = ids.clone(), g.clone(), E0.to(dev())
+    graph.step(ids3, g3, Ec, 0.1)
+    eager.step(ids3, g3, Ea.copy_(E0.to(dev())), 0.1)
+    torch.cuda.synchronize()
+    assert torch.equal(Ea, Ec)
+    eager.close()
+    graph.close()
+
+
 def test_deterministic_run_to_run(lm):
     cfg = synth.CONFIGS["1b"]
     J = to_dev_ids(synth.ids_for(cfg, 0))
