@@ -71,9 +71,8 @@ typedef enum {
 #define LMSCALE_FLAG_NO_COMM 1u /* no NCCL communicator: staged calls only (test emulation of G ranks) */
 #define LMSCALE_FLAG_TIMING 2u  /* record CUDA events around each phase; lmscale_get_stats reports them */
 #define LMSCALE_FLAG_GRAPH 4u   /* lmscale_step captures the whole step into a CUDA graph (once per
-                                   (ids, grad, table, k, lr) tuple) and replays it; applies when the
-                                   step needs no host round trip (world == 1, or the fused NVLS
-                                   S5+S6 kernel) and num_unique_out == NULL */
+                                   (ids, grad, table, k, lr) tuple) and replays it; applies with
+                                   world == 1 and num_unique_out == NULL (no host round trip) */
 
 typedef struct {
   int64_t vocab;      /* |V| >= 1 */

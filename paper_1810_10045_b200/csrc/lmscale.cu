@@ -768,7 +768,7 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
   // fused NVLS kernel is available, so it is captured once per argument tuple
   // and replayed (one launch instead of ~5 kernels + events + NCCL calls).
   if (ctx && (ctx->cfg.flags & LMSCALE_FLAG_GRAPH) && !num_unique_out &&
-      (ctx->cfg.world == 1 || ctx->nvls)) {
+      ctx->cfg.world == 1) {
     lmscale_status st0 = check_ids_args(ctx, ids, k);
     if (st0) return st0;
     cudaStream_t s = S(stream);
