@@ -286,19 +286,37 @@ def main():
     # per-phase device times (median over timed steps), max over ranks
     ph = {k: max_over_ranks(statistics.median(v), dev) for k, v in phase.items() if v}
     hbm_peak, peak_kind = peaks()
-    scatter_bytes = 4 * cfg.K * cfg.D + 4 * ug * cfg.D
-    update_bytes = 12 * ug * cfg.D
+    st_last = ctx.stats()
+    D = cfg.D
+    if world == 1:
+        # S4 + fixup + S6 in one cooperative launch (the all-reduce is the identity)
+        kname = "k_scatter (S4 segmented scatter-add + fused S6 row update, world 1)"
+        scatter_bytes = 4 * cfg.K * D + 8 * ug * D   # grad read + E rows read/write
+    else:
+        kname = "k_scatter (S4 segmented scatter-add)"
+        scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
     scatter_us = ph["us_scatter"]
-    roof = {"kernel": "k_scatter (S4 segmented scatter-add)", "bound": "hbm",
+    roof = {"kernel": kname, "bound": "hbm",
             "achieved": scatter_bytes / (scatter_us * 1e-6) / 1e9, "peak": hbm_peak,
             "unit": "GB/s", "peak_kind": peak_kind,
             "bytes_per_launch": scatter_bytes, "us_per_launch": scatter_us}
     roof["frac"] = roof["achieved"] / hbm_peak
-    roof["traffic"] = ncu_traffic(cfg.name)
-    upd = {"kernel": "k_update (S6 row update)", "achieved": update_bytes /
-           (ph["us_update"] * 1e-6) / 1e9, "bytes_per_launch": update_bytes,
-           "us_per_launch": ph["us_update"]}
-    upd["frac"] = upd["achieved"] / hbm_peak
+    roof["traffic"] = ncu_traffic(cfg.name, world)
+    if world == 1:
+        upd = {"kernel": "S6 fused into k_scatter (world 1)"}
+    elif st_last.get("fused_s5_s6"):
+        nvl = (1 + 1 / world) * 4 * ug * D   # bytes per direction per GPU
+        upd = {"kernel": "k_nvls_update (S5+S6 fused, NVLS multimem)", "bound": "nvlink",
+               "bytes_per_direction": nvl, "us_per_launch": ph["us_allreduce"],
+               "achieved": nvl / (ph["us_allreduce"] * 1e-6) / 1e9, "peak": 770.0,
+               "peak_kind": "guide: measured peer copy per direction (900 nominal)"}
+        upd["frac"] = upd["achieved"] / upd["peak"]
+    else:
+        update_bytes = 12 * ug * D
+        upd = {"kernel": "k_update (S6 row update)", "achieved": update_bytes /
+               (ph["us_update"] * 1e-6) / 1e9, "bytes_per_launch": update_bytes,
+               "us_per_launch": ph["us_update"]}
+        upd["frac"] = upd["achieved"] / hbm_peak
 
     # ---- dense comparison path (S0), same inputs, separate table copy
     dense = None
@@ -351,7 +369,7 @@ def main():
                 "counter-hash fp32 gradients/table; no datasets)",
                 "config": config_dict(cfg, args, world),
                 "U_local": info.get("u_local"), "U_global": ug, "E_U_global_closed_form": eu,
-                "phases_us_median": ph, "roofline": roof, "roofline_update": upd,
+                "phases_us_median": ph, "roofline": roof, "roofline_s5_s6": upd,
                 "dense_baseline": dense, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": sync_launches, "gpu_launches_per_step": sync_launches / args.steps,
                 "library": lmscale.version()}
@@ -362,14 +380,14 @@ def main():
         dist.destroy_process_group()
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, world):
     """dram read+write bytes per launch of k_scatter from the committed ncu
-    --set full summary (profiles/), or None."""
+    --set full summary (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(workload, {}).get("k_scatter")
+        return d.get(f"{workload}/G{world}", {}).get("k_scatter")
     except Exception:
         return None
 

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   if (cr == 0 && tid == 0) {
     a.sc->err = 0u;
     a.sc->u_local = 0;
+    a.sc->fixcount = 0u;
     if (a.sc3) {
       a.sc3->err = 0u;
       a.sc3->u_global = 0;

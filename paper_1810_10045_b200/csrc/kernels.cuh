@@ -16,7 +16,7 @@ constexpr int SC_ZGROUP = 32;
 struct Sc1 {
   int64_t u_local;
   uint32_t err;        // bit 0: an id >= vocab seen by S1
-  uint32_t pad;
+  uint32_t fixcount;   // S4: runs cut by chunk boundaries (zeroed by S1)
 };
 // Per-step device scalars of S3 (zeroed at the start of S3).
 struct Sc3 {
@@ -108,6 +108,12 @@ struct ScatterArgs {
   const uint32_t* lbits;  // local presence bitmap
   const Sc3* sc3;         // U_g
   const Sc1* sc1;         // U_i
+  Sc1* sc1w;              // fixup list counter
+  int32_t* fixlist;       // owner chunks of cut runs
+  int fix_cap;
+  int zero_rows;          // 0: every slot is present locally (world 1)
+  float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
+  float lr;
   float* M;               // U_g x D
   float* partial;         // 2 * nchunks x D
   int K;
@@ -115,8 +121,8 @@ struct ScatterArgs {
   int64_t ug_cap;         // capacity bound on U_g (sizes the grid)
   int num_sms;
 };
-void launch_scatter(const ScatterArgs& a, cudaStream_t s);
-void launch_fixup(const ScatterArgs& a, cudaStream_t s);
+// One cooperative launch: scatter, cut-run fixup, and (a.table) the world-1 S6.
+cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
 
 // ---- S6 / S0 --------------------------------------------------------------
 // n_dev != nullptr: the row count is read on the device (min(n, *n_dev)); n

@@ -58,7 +58,7 @@ struct lmscale_ctx {
   void* base = nullptr;
   size_t ws_bytes = 0;
   uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot;
-  int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
+  int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g, *fixlist;
   float* M = nullptr;
   float* partial;
   bool m_nccl = false;
@@ -267,6 +267,12 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.sc1 = ctx->sc1;
   a.M = ctx->M;
   a.partial = ctx->partial;
+  a.sc1w = ctx->sc1;
+  a.fixlist = ctx->fixlist;
+  a.fix_cap = (int)ctx->nchunks;
+  a.zero_rows = 1;
+  a.table = nullptr;
+  a.lr = 0.f;
   a.K = (int)ctx->last_k;
   a.D = (int)ctx->cfg.dim;
   a.ug_cap = std::min<int64_t>(ctx->last_n, ctx->cfg.vocab);
@@ -274,13 +280,16 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   return a;
 }
 
-lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s) {
+// S4 (+ the world-1 S6 when table != nullptr): one cooperative launch.
+lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
+                      float* table = nullptr, float lr = 0.f, bool zero_rows = true) {
   ScatterArgs a = scatter_args(ctx, grad);
-  launch_scatter(a, s);
+  a.table = table;
+  a.lr = lr;
+  a.zero_rows = zero_rows ? 1 : 0;
+  CK(launch_scatter(a, s));
   LAUNCHED(1);
   rec(ctx, EV_SCATTER_END, s);
-  launch_fixup(a, s);
-  LAUNCHED(1);
   return LMSCALE_OK;
 }
 
@@ -365,7 +374,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_vals_b = take(4 * K), o_segidx = take(4 * K), o_inverse = take(4 * K),
            o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)), o_counts = take(4 * K),
            o_l2g = take(4 * K), o_wrank = take(4 * ctx->W), o_I = take(4 * ctx->NI),
-           o_ihat = take(4 * ctx->ucap);
+           o_ihat = take(4 * ctx->ucap), o_fix = take(4 * ctx->nchunks);
     size_t o_sc3 = take(sizeof(Sc3) + sizeof(Sc1)), o_sc1 = o_sc3 + sizeof(Sc3),
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
            o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
@@ -393,6 +402,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->wrank = (uint32_t*)(b + o_wrank);
     ctx->I = (uint32_t*)(b + o_I);
     ctx->ihat = (uint32_t*)(b + o_ihat);
+    ctx->fixlist = (int32_t*)(b + o_fix);
     ctx->sc1 = (Sc1*)(b + o_sc1);
     ctx->sc3 = (Sc3*)(b + o_sc3);
     ctx->cT = (uint32_t*)(b + o_cT);
@@ -645,8 +655,10 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
                        ctx->s_copy));
     CK(cudaEventRecord(ctx->ev_copy, ctx->s_copy));
   }
-  // S4: segmented scatter-add into M.
-  st = run_s4(ctx, grad, s);
+  // S4: segmented scatter-add into M; with one rank
+  // the all-reduce is the identity and S6 rides in the same launch.
+  const bool fuse_s6 = (G == 1 && table != nullptr);
+  st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*zero_rows=*/G > 1);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
   if (G > 1 && table && ctx->nvls) {
@@ -692,12 +704,9 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   }
   ctx->fused_last = false;
   if (G == 1 && table && !need_host_ug) {
-    // S6 straight away with the device-side count: no host round trip.
+    // S6 already ran inside the S4 launch: no host round trip.
     rec(ctx, EV_AR_END, s);
     rec(ctx, EV_UPD_BEGIN, s);
-    launch_update(table, (int)D, ctx->ihat, ctx->M, ctx->ucap, &ctx->sc3->u_global, lr,
-                  ctx->num_sms, s);
-    LAUNCHED(1);
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
@@ -729,8 +738,10 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   rec(ctx, EV_AR_END, s);
   if (table) {
     rec(ctx, EV_UPD_BEGIN, s);
-    launch_update(table, (int)D, ctx->ihat, ctx->M, ug, nullptr, lr, ctx->num_sms, s);
-    if (ug > 0) LAUNCHED(1);
+    if (!fuse_s6) {
+      launch_update(table, (int)D, ctx->ihat, ctx->M, ug, nullptr, lr, ctx->num_sms, s);
+      if (ug > 0) LAUNCHED(1);
+    }
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
   }

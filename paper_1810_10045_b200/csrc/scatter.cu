@@ -12,8 +12,12 @@
 // partials in a fixed order (deterministic, no atomics) and writes its M row.
 // Slots whose word is absent on this rank are written as zeros by extra work
 // items, so every one of the U_g rows is stored exactly once (no memset).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace lms {
 
@@ -50,7 +54,6 @@ struct Vec<float> {
 
 constexpr int SC_THREADS = 256;
 constexpr unsigned FULL_MASK = 0xffffffffu;
-constexpr int FX_THREADS = 512;
 
 }  // namespace
 
@@ -109,12 +112,19 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
         if (last || ((hmask >> (p + 1)) & 1u)) {
           const int slot = __shfl_sync(FULL_MASK, my_slot, p);
           T* dst;
-          if (seg_first && split_left)
+          if (seg_first && split_left) {
             dst = P + (size_t)(2 * c) * C;
-          else if (last && split_right)
+          } else if (last && split_right) {
             dst = P + (size_t)(2 * c + 1) * C;
-          else
+            // this chunk holds the start of a run cut by its end: it owns the
+            // run's fixup (listed once, by column block 0)
+            if (col0 == lane && lane == 0) {
+              const uint32_t idx = atomicAdd(&a.sc1w->fixcount, 1u);
+              if (idx < (uint32_t)a.fix_cap) a.fixlist[idx] = c;
+            }
+          } else {
             dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
+          }
           if (dst) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
@@ -131,15 +141,80 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   }
 }
 
+// Phase 2 (fixup) for one (owner chunk c, column block): sum the run's
+// partials P[2c+1] (tail of c) and P[2c'] (heads of c < c' <= c1) in a fixed
+// order -- warp w sums partials w, w+8, ...; warps are combined in warp order
+// through shared memory -- and store the run's row (deterministic).
+template <typename T, int NV>
+__device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * NV], int c,
+                                           int cb, int C) {
+  using V = Vec<T>;
+  constexpr int NWF = SC_THREADS / 32;
+  constexpr int UNR = 4;
+  const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
+  const T* P = reinterpret_cast<const T*>(a.partial);
+  T* M = reinterpret_cast<T*>(a.M);
+  const int iend = min(a.K, (c + 1) * SC_CHUNK);
+  const int u = __ldcg(a.segidx + iend - 1);
+  const int c1 = (__ldcg(a.lstart + u + 1) - 1) / SC_CHUNK;
+  const int np = c1 - c + 1;
+  const int slot = __ldcg(a.l2g + u);
+  const int col0 = cb * 32 * NV + lane;
+  T acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+  for (int k0 = warp; k0 < np; k0 += NWF * UNR) {
+    T r[UNR][NV];
+#pragma unroll
+    for (int q = 0; q < UNR; ++q) {
+      const int k = k0 + q * NWF;
+      const size_t prow = k == 0 ? (size_t)(2 * c + 1) : (size_t)(2 * (c + k));
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int col = col0 + v * 32;
+        r[q][v] = V::zero();
+        if (k < np && col < C) r[q][v] = V::ld_l2(P + prow * C + col);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UNR; ++q)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) red[warp][v * 32 + lane] = acc[v];
+  __syncthreads();
+  if (warp == 0 && slot >= 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      T sum = red[0][v * 32 + lane];
+#pragma unroll
+      for (int w = 1; w < NWF; ++w) sum = V::add(sum, red[w][v * 32 + lane]);
+      const int col = col0 + v * 32;
+      if (col < C) V::st(M + (size_t)slot * C + col, sum);
+    }
+  }
+  __syncthreads();
+}
+
+// S4 as one cooperative persistent kernel:
+//   phase 1  chunk items (segment sums -> M, partials for cut runs) and
+//            zero-row items; owners of cut runs append to the fixup list;
+//   phase 2  (after a grid barrier) the listed runs' partial sums -> M;
+//   phase 3  (world 1 only, after a grid barrier) S6: E[I^[r]] -= lr * M[r]
+//            -- with one rank the all-reduce is the identity, so the update
+//            rides in the same launch.
 template <typename T, int NV, int UNR>
 __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   using V = Vec<T>;
+  __shared__ T red[SC_THREADS / 32][32 * NV];
+  cg::grid_group grid = cg::this_grid();
   const int K = a.K;
   const int C = a.D / V::W;  // vectors per row
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
   const int nchunks = (K + SC_CHUNK - 1) / SC_CHUNK;
   const int64_t Ug = a.sc3->u_global;
-  const int64_t nz = (Ug + SC_ZGROUP - 1) / SC_ZGROUP;
+  const int64_t nz = a.zero_rows ? (Ug + SC_ZGROUP - 1) / SC_ZGROUP : 0;
   const int64_t items = ((int64_t)nchunks + nz) * ncb;
   const int lane = (int)lane_id();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -181,73 +256,34 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
       }
     }
   }
-}
+  grid.sync();
 
-// Sum the partials of every run cut by a chunk boundary.  Work item =
-// (chunk c that holds the START of a run continuing into chunk c+1, column
-// block); the run's partials are P[2c+1] (tail of c) and P[2c'] (head) for
-// c < c' <= c1.  Warp w sums partials w, w+16, ... in order; warps are then
-// combined in warp order through shared memory (deterministic).
-template <typename T, int NV>
-__global__ void __launch_bounds__(FX_THREADS) k_fixup(ScatterArgs a) {
-  using V = Vec<T>;
-  constexpr int NWF = FX_THREADS / 32;
-  constexpr int UNR = 4;
-  __shared__ T red[NWF][32 * NV];
-  const int K = a.K;
-  const int C = a.D / V::W;
-  const int ncb = (C + 32 * NV - 1) / (32 * NV);
-  const int nchunks = (K + SC_CHUNK - 1) / SC_CHUNK;
-  const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
-  const T* P = reinterpret_cast<const T*>(a.partial);
-  T* M = reinterpret_cast<T*>(a.M);
-  const int64_t items = (int64_t)nchunks * ncb;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int c = (int)(it / ncb);
-    const int cb = (int)(it % ncb);
-    const int iend = min(K, (c + 1) * SC_CHUNK);
-    if (iend >= K) continue;
-    const int u = __ldg(a.segidx + iend - 1);
-    if (__ldg(a.segidx + iend) != u) continue;      // run ends inside chunk c
-    const int s0 = __ldg(a.lstart + u);
-    if (s0 < c * SC_CHUNK) continue;                 // run owned by an earlier chunk
-    const int c1 = (__ldg(a.lstart + u + 1) - 1) / SC_CHUNK;
-    const int np = c1 - c + 1;
-    const int slot = __ldg(a.l2g + u);
-    const int col0 = cb * 32 * NV + lane;
-    T acc[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-    for (int k0 = warp; k0 < np; k0 += NWF * UNR) {
-      T r[UNR][NV];
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int k = k0 + q * NWF;
-        const size_t prow = k == 0 ? (size_t)(2 * c + 1) : (size_t)(2 * (c + k));
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int col = col0 + v * 32;
-          r[q][v] = (k < np && col < C) ? V::ld_l2(P + prow * C + col) : V::zero();
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
+  // phase 2: runs cut by chunk boundaries
+  const int nfix = (int)min(__ldcg(&a.sc1w->fixcount), (uint32_t)a.fix_cap);
+  for (int64_t it = blockIdx.x; it < (int64_t)nfix * ncb; it += gridDim.x)
+    fixup_item<T, NV>(a, red, __ldcg(a.fixlist + it / ncb), (int)(it % ncb), C);
+
+  if (!a.table) return;
+  grid.sync();
+
+  // phase 3 (world 1): S6 row update, warp per row
+  T* E = reinterpret_cast<T*>(a.table);
+  const float lr = a.lr;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Ug; r += nwarps) {
+    const uint32_t w = __ldg(a.ihat + r);
+    const T* src = M + (size_t)r * C;
+    T* dst = E + (size_t)w * C;
+    int col = lane;
+    for (; col + 96 < C; col += 128) {
+      const T m0 = V::ld_l2(src + col), m1 = V::ld_l2(src + col + 32);
+      const T m2 = V::ld_l2(src + col + 64), m3 = V::ld_l2(src + col + 96);
+      const T e0 = dst[col], e1 = dst[col + 32], e2 = dst[col + 64], e3 = dst[col + 96];
+      V::st(dst + col, V::fma(-lr, m0, e0));
+      V::st(dst + col + 32, V::fma(-lr, m1, e1));
+      V::st(dst + col + 64, V::fma(-lr, m2, e2));
+      V::st(dst + col + 96, V::fma(-lr, m3, e3));
     }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) red[warp][v * 32 + lane] = acc[v];
-    __syncthreads();
-    if (warp == 0 && slot >= 0) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        T s = red[0][v * 32 + lane];
-        for (int w = 1; w < NWF; ++w) s = V::add(s, red[w][v * 32 + lane]);
-        const int col = col0 + v * 32;
-        if (col < C) V::st(M + (size_t)slot * C + col, s);
-      }
-    }
-    __syncthreads();
+    for (; col < C; col += 32) V::st(dst + col, V::fma(-lr, V::ld_l2(src + col), dst[col]));
   }
 }
 
@@ -261,13 +297,7 @@ bool vec_ok(const ScatterArgs& a) {
 }  // namespace
 
 template <typename T, int NV, int UNR>
-static void scatter_t(const ScatterArgs& a, cudaStream_t s) {
-  const int C = a.D / Vec<T>::W;
-  const int ncb = (C + 32 * NV - 1) / (32 * NV);
-  const int64_t nchunks = (a.K + SC_CHUNK - 1) / SC_CHUNK;
-  const int64_t nz = (a.ug_cap + SC_ZGROUP - 1) / SC_ZGROUP;
-  const int64_t warps = (nchunks + nz) * ncb;
-  int64_t blocks = (warps * 32 + SC_THREADS - 1) / SC_THREADS;
+static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   static int occ = 0;  // resident CTAs per SM for this instantiation (persistent grid)
   if (!occ) {
     max_carveout((const void*)k_scatter<T, NV, UNR>);
@@ -275,52 +305,28 @@ static void scatter_t(const ScatterArgs& a, cudaStream_t s) {
                                                       0) != cudaSuccess || occ < 1)
       occ = 1;
   }
-  const int64_t cap = (int64_t)a.num_sms * occ;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  k_scatter<T, NV, UNR><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
-}
-
-template <typename T, int NV>
-static void fixup_t(const ScatterArgs& a, cudaStream_t s) {
   const int C = a.D / Vec<T>::W;
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
   const int64_t nchunks = (a.K + SC_CHUNK - 1) / SC_CHUNK;
-  int64_t blocks = nchunks * ncb;
-  const int64_t cap = (int64_t)a.num_sms * 4;
+  const int64_t nz = a.zero_rows ? (a.ug_cap + SC_ZGROUP - 1) / SC_ZGROUP : 0;
+  int64_t blocks = ((nchunks + nz) * ncb * 32 + SC_THREADS - 1) / SC_THREADS;
+  const int64_t cap = (int64_t)a.num_sms * occ;
   if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  static bool once = (max_carveout((const void*)k_fixup<T, NV>), true);
-  (void)once;
-  k_fixup<T, NV><<<(unsigned)blocks, FX_THREADS, 0, s>>>(a);
+  if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phases 2/3 want a wide grid
+  ScatterArgs args = a;
+  void* kargs[] = {(void*)&args};
+  return cudaLaunchCooperativeKernel((void*)k_scatter<T, NV, UNR>, dim3((unsigned)blocks),
+                                     dim3(SC_THREADS), kargs, 0, s);
 }
 
-void launch_scatter(const ScatterArgs& a, cudaStream_t s) {
+cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
   if (vec_ok<float4>(a)) {
     const int C = a.D / 4;
-    if (C >= 128)
-      scatter_t<float4, 4, 4>(a, s);
-    else if (C >= 64)
-      scatter_t<float4, 2, 4>(a, s);
-    else
-      scatter_t<float4, 1, 4>(a, s);
-  } else {
-    scatter_t<float, 4, 4>(a, s);
+    if (C >= 128) return scatter_t<float4, 4, 4>(a, s);
+    if (C >= 64) return scatter_t<float4, 2, 4>(a, s);
+    return scatter_t<float4, 1, 4>(a, s);
   }
-}
-
-void launch_fixup(const ScatterArgs& a, cudaStream_t s) {
-  if (vec_ok<float4>(a)) {
-    const int C = a.D / 4;
-    if (C >= 128)
-      fixup_t<float4, 4>(a, s);
-    else if (C >= 64)
-      fixup_t<float4, 2>(a, s);
-    else
-      fixup_t<float4, 1>(a, s);
-  } else {
-    fixup_t<float, 4>(a, s);
-  }
+  return scatter_t<float, 4, 4>(a, s);
 }
 
 // ------------------------------------------------------------------- S6
