@@ -288,13 +288,8 @@ def main():
     hbm_peak, peak_kind = peaks()
     st_last = ctx.stats()
     D = cfg.D
-    if world == 1:
-        # S4 + fixup + S6 in one cooperative launch (the all-reduce is the identity)
-        kname = "k_scatter (S4 segmented scatter-add + fused S6 row update, world 1)"
-        scatter_bytes = 4 * cfg.K * D + 8 * ug * D   # grad read + E rows read/write
-    else:
-        kname = "k_scatter (S4 segmented scatter-add)"
-        scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
+    kname = "k_scatter (S4 segmented scatter-add + cut-run fixup, one cooperative launch)"
+    scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
     scatter_us = ph["us_scatter"]
     roof = {"kernel": kname, "bound": "hbm",
             "achieved": scatter_bytes / (scatter_us * 1e-6) / 1e9, "peak": hbm_peak,
@@ -302,9 +297,7 @@ def main():
             "bytes_per_launch": scatter_bytes, "us_per_launch": scatter_us}
     roof["frac"] = roof["achieved"] / hbm_peak
     roof["traffic"] = ncu_traffic(cfg.name, world)
-    if world == 1:
-        upd = {"kernel": "S6 fused into k_scatter (world 1)"}
-    elif st_last.get("fused_s5_s6"):
+    if st_last.get("fused_s5_s6"):
         nvl = (1 + 1 / world) * 4 * ug * D   # bytes per direction per GPU
         upd = {"kernel": "k_nvls_update (S5+S6 fused, NVLS multimem)", "bound": "nvlink",
                "bytes_per_direction": nvl, "us_per_launch": ph["us_allreduce"],

@@ -657,7 +657,9 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   }
   // S4: segmented scatter-add into M; with one rank
   // the all-reduce is the identity and S6 rides in the same launch.
-  const bool fuse_s6 = (G == 1 && table != nullptr);
+  // (fusing S6 into S4's cooperative kernel at world 1 was measured slower
+  // than the separate, higher-occupancy update launch; kept separate)
+  const bool fuse_s6 = false;
   st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*zero_rows=*/G > 1);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
@@ -704,9 +706,12 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   }
   ctx->fused_last = false;
   if (G == 1 && table && !need_host_ug) {
-    // S6 already ran inside the S4 launch: no host round trip.
+    // S6 straight away with the device-side count: no host round trip.
     rec(ctx, EV_AR_END, s);
     rec(ctx, EV_UPD_BEGIN, s);
+    launch_update(table, (int)D, ctx->ihat, ctx->M, ctx->ucap, &ctx->sc3->u_global, lr,
+                  ctx->num_sms, s);
+    LAUNCHED(1);
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);

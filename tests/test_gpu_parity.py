@@ -212,7 +212,7 @@ def test_graph_replay_equals_eager(lm):
         torch.cuda.synchronize()
         assert torch.equal(Ea, Eb), step
     st = graph.stats()
-    assert st["us_scatter"] > 0 and st["kernels_last_call"] >= 3
+    assert st["us_scatter"] > 0 and st["kernels_last_call"] >= 2
     # different buffers: re-capture
     ids3, g3, Ec = ids.clone(), g.clone(), E0.to(dev())
     graph.step(ids3, g3, Ec, 0.1)
