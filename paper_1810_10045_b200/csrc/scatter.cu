@@ -75,7 +75,8 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   }
   const int prev_u = i0 > 0 ? __ldg(a.segidx + i0 - 1) : -1;
   const int next_u = i0 + n < K ? __ldg(a.segidx + i0 + n) : -1;
-  if (FULL || lane < n) my_slot = __ldg(a.l2g + my_u);
+  // world 1: I^ = J^, so the slot is the run index itself (no dependent load)
+  if (FULL || lane < n) my_slot = a.zero_rows ? __ldg(a.l2g + my_u) : my_u;
   const int up = __shfl_up_sync(FULL_MASK, my_u, 1);
   const unsigned hmask = __ballot_sync(FULL_MASK, (FULL || lane < n) && (lane == 0 || my_u != up));
   const bool split_left = __shfl_sync(FULL_MASK, my_u, 0) == prev_u;
@@ -322,8 +323,7 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
   if (vec_ok<float4>(a)) {
     const int C = a.D / 4;
-    if (C >= 128) return scatter_t<float4, 4, 4>(a, s);
-    if (C >= 64) return scatter_t<float4, 2, 4>(a, s);
+    if (C >= 64) return scatter_t<float4, 2, 8>(a, s);
     return scatter_t<float4, 1, 4>(a, s);
   }
   return scatter_t<float, 4, 4>(a, s);

@@ -40,6 +40,60 @@ __global__ void k_rankloop(uint32_t* out, int iters) {
   if (acc == 12345) out[1000] = acc;
 }
 
+__global__ void k_rankloop_atom(uint32_t* out, int iters) {
+  __shared__ uint32_t cnt[16][512];
+  for (int i = threadIdx.x; i < 16 * 512; i += blockDim.x) (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = threadIdx.x * 2654435761u, acc = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    x = x * 1664525u + 1013904223u;
+    uint32_t d = (x >> 23) & 511u;
+    unsigned m = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(m) - 1;
+    uint32_t old = 0;
+    if (lane == leader) old = atomicAdd(&cnt[warp][d], (uint32_t)__popc(m));
+    old = __shfl_sync(0xffffffffu, old, leader);
+    acc += old + __popc(m & ((1u << lane) - 1));
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = (uint32_t)(t1 - t0);
+  if (acc == 12345) out[1000] = acc;
+}
+
+// 8 items per thread: all matches first, then the counter updates
+__global__ void k_rankloop_batch(uint32_t* out, int iters) {
+  __shared__ uint32_t cnt[16][512];
+  for (int i = threadIdx.x; i < 16 * 512; i += blockDim.x) (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = threadIdx.x * 2654435761u, acc = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; i += 8) {
+    uint32_t d[8];
+    unsigned m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      x = x * 1664525u + 1013904223u;
+      d[j] = (x >> 23) & 511u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = __match_any_sync(0xffffffffu, d[j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int leader = __ffs(m[j]) - 1;
+      uint32_t old = 0;
+      if (lane == leader) old = atomicAdd(&cnt[warp][d[j]], (uint32_t)__popc(m[j]));
+      old = __shfl_sync(0xffffffffu, old, leader);
+      acc += old + __popc(m[j] & ((1u << lane) - 1));
+    }
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = (uint32_t)(t1 - t0);
+  if (acc == 12345) out[1000] = acc;
+}
+
 __global__ void k_cluster_sync(uint32_t* out, int iters) {
   cg::cluster_group cl = cg::this_cluster();
   long long t0 = clock64();
@@ -94,6 +148,15 @@ int main() {
   k_rankloop<<<8, 512>>>(d, it);
   cudaMemcpy(h, d, 4, cudaMemcpyDeviceToHost);
   printf("rank loop (match+lds+2 syncwarp+sts): %.1f cyc/iter (16 warps/SM)\n", h[0] / (double)it);
+  k_rankloop_atom<<<8, 512>>>(d, it);
+  cudaMemcpy(h, d, 4, cudaMemcpyDeviceToHost);
+  printf("rank loop atomic+shfl: %.1f cyc/iter (16 warps/SM)\n", h[0] / (double)it);
+  k_rankloop_batch<<<8, 512>>>(d, it);
+  cudaMemcpy(h, d, 4, cudaMemcpyDeviceToHost);
+  printf("rank loop batched matches + atomic+shfl: %.1f cyc/iter (16 warps/SM)\n", h[0] / (double)it);
+  k_rankloop<<<8, 256>>>(d, it);
+  cudaMemcpy(h, d, 4, cudaMemcpyDeviceToHost);
+  printf("rank loop orig: %.1f cyc/iter (8 warps/SM)\n", h[0] / (double)it);
   for (int C : {2, 8, 16}) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
