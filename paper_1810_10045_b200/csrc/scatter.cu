@@ -323,7 +323,8 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
   if (vec_ok<float4>(a)) {
     const int C = a.D / 4;
-    if (C >= 64) return scatter_t<float4, 2, 8>(a, s);
+    if (C >= 128) return scatter_t<float4, 4, 4>(a, s);
+    if (C >= 64) return scatter_t<float4, 2, 4>(a, s);
     return scatter_t<float4, 1, 4>(a, s);
   }
   return scatter_t<float, 4, 4>(a, s);
