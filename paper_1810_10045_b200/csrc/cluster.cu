@@ -29,10 +29,13 @@ __device__ __forceinline__ void cstamp(unsigned long long* tr, int i) {
 }
 constexpr int CT = CL_THREADS;
 constexpr int NW = CL_THREADS / 32;
-constexpr int IT = CL_TILE / CL_THREADS;  // 8 keys per thread
 }  // namespace
 
+// IT keys per thread: tile = 512 * IT keys per CTA (IT = 4 spreads K <= 32K
+// over up to 16 SMs; the ranking is match_any-throughput-bound per SM).
+template <int IT>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
+  constexpr int CL_TILE = CL_THREADS * IT;
   extern __shared__ uint32_t sm[];
   __shared__ uint32_t s_scan[32];
   __shared__ uint32_t s_heads;
@@ -41,8 +44,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   const int C = (int)cl.num_blocks();
   const int ndig = 1 << a.bits;
   // (key, val) pairs, ping-pong: one 8-byte DSMEM store per element
-  uint2* kv[2] = {reinterpret_cast<uint2*>(sm), reinterpret_cast<uint2*>(sm + 2 * CL_TILE)};
-  uint32_t* s_cnt = sm + 4 * CL_TILE;   // [NW][ndig]
+  uint2* kv[2] = {reinterpret_cast<uint2*>(sm), reinterpret_cast<uint2*>(sm + 2 * CL_MAX_TILE)};
+  uint32_t* s_cnt = sm + 4 * CL_MAX_TILE;  // [NW][ndig]
   uint32_t* s_tot = s_cnt + NW * ndig;  // [ndig] this tile's digit totals
   uint32_t* s_base = s_tot + ndig;      // [ndig]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -256,25 +259,31 @@ SortPlan make_cluster_plan(uint64_t vocab) {
 }
 
 size_t cluster_smem_bytes(int bits) {
-  return (size_t)(4 * CL_TILE + (NW + 2) * (1 << bits)) * 4;
+  return (size_t)(4 * CL_MAX_TILE + (NW + 2) * (1 << bits)) * 4;
 }
+
+static int cluster_items(int K) { return K <= CL_MAX_CTAS * CL_THREADS * 4 ? 4 : 8; }
 
 bool cluster_s1_ok(int K) {
   static int ok = -1;
   if (ok < 0) {
-    ok = cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                 cudaSuccess &&
-         cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)cluster_smem_bytes(CL_MAX_BITS)) == cudaSuccess &&
-         cudaFuncSetAttribute(k_s1_cluster, cudaFuncAttributePreferredSharedMemoryCarveout,
-                              100) == cudaSuccess;
+    ok = 1;
+    for (const void* f : {(const void*)k_s1_cluster<4>, (const void*)k_s1_cluster<8>}) {
+      ok &= cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess &&
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cluster_smem_bytes(CL_MAX_BITS)) == cudaSuccess;
+      max_carveout(f);
+    }
     if (!ok) cudaGetLastError();
   }
-  return ok && K >= 1 && K <= CL_MAX_CTAS * CL_TILE;
+  return ok && K >= 1 && K <= CL_MAX_CTAS * CL_MAX_TILE;
 }
 
 cudaError_t launch_s1_cluster(const S1Args& a, cudaStream_t s) {
-  const int C = (a.K + CL_TILE - 1) / CL_TILE;
+  const int it = cluster_items(a.K);
+  const int tile = CL_THREADS * it;
+  const int C = (a.K + tile - 1) / tile;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(CL_THREADS);
@@ -287,7 +296,8 @@ cudaError_t launch_s1_cluster(const S1Args& a, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_s1_cluster, a);
+  return it == 4 ? cudaLaunchKernelEx(&cfg, k_s1_cluster<4>, a)
+                 : cudaLaunchKernelEx(&cfg, k_s1_cluster<8>, a);
 }
 
 }  // namespace lms

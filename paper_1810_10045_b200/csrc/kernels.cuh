@@ -79,9 +79,9 @@ struct S3Args {
 };
 SortPlan make_coop_plan(uint64_t vocab);
 
-// ---- cluster S1 (cluster.cu): K <= CL_MAX_CTAS * CL_TILE, one cluster ------
+// ---- cluster S1 (cluster.cu): K <= CL_MAX_CTAS * CL_MAX_TILE, one cluster --
 constexpr int CL_THREADS = 512;
-constexpr int CL_TILE = 4096;
+constexpr int CL_MAX_TILE = 4096;  // keys per CTA (512 threads x 8)
 constexpr int CL_MAX_BITS = 10;
 constexpr int CL_MAX_CTAS = 16;
 SortPlan make_cluster_plan(uint64_t vocab);
