@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   constexpr int CL_TILE = CL_THREADS * IT;
   extern __shared__ uint32_t sm[];
   __shared__ uint32_t s_scan[32];
-  __shared__ uint32_t s_heads;
+  __shared__ uint32_t s_heads, s_rtot, s_roff;
   cg::cluster_group cl = cg::this_cluster();
   const int cr = (int)cl.block_rank();
   const int C = (int)cl.num_blocks();
@@ -47,7 +47,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   uint2* kv[2] = {reinterpret_cast<uint2*>(sm), reinterpret_cast<uint2*>(sm + 2 * CL_MAX_TILE)};
   uint32_t* s_cnt = sm + 4 * CL_MAX_TILE;  // [NW][ndig]
   uint32_t* s_tot = s_cnt + NW * ndig;  // [ndig] this tile's digit totals
-  uint32_t* s_base = s_tot + ndig;      // [ndig]
+  uint32_t* s_base = s_tot + ndig;      // [ndig]  written remotely by the digit owners
+  uint32_t* s_tmp = s_base + ndig;      // [ndig]  owner-side scratch (C x range)
+  uint32_t* s_dex = s_tmp + ndig + 32;  // [ndig]  (nr * C <= ndig + C)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.K;
   const int t0 = cr * CL_TILE;  // first global sorted position of this CTA
@@ -120,44 +122,43 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
     cstamp(a.trace, 1 + 4 * p);
     cl.sync();  // every CTA's digit totals are published
     cstamp(a.trace, 2 + 4 * p);
-    const int dpt = ndig > CT ? ndig / CT : 1;
-    const int d0 = tid * dpt;
-    uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
-    if (d0 < ndig) {
-      if (dpt == 2) {
-        uint2 v[CL_MAX_CTAS];
-#pragma unroll
-        for (int c = 0; c < CL_MAX_CTAS; ++c)
-          if (c < C) v[c] = *reinterpret_cast<const uint2*>(cl.map_shared_rank(s_tot, c) + d0);
-#pragma unroll
-        for (int c = 0; c < CL_MAX_CTAS; ++c)
-          if (c < C) {
-            tot[0] += v[c].x;
-            tot[1] += v[c].y;
-            if (c < cr) {
-              pre[0] += v[c].x;
-              pre[1] += v[c].y;
-            }
-          }
-      } else {
+    {
+      // CTA cr owns digits [r0, r1): it reads that range from every CTA once,
+      // forms the per-CTA exclusive prefixes and the digit totals, and after
+      // the range offsets are known writes every CTA's bases remotely.
+      const int r0 = (int)((int64_t)ndig * cr / C), r1 = (int)((int64_t)ndig * (cr + 1) / C);
+      const int nr = r1 - r0;
+      for (int i = tid; i < nr * C; i += CT) {
+        const int c = i / nr, dl = i % nr;
+        s_tmp[c * nr + dl] = cl.map_shared_rank(s_tot, c)[r0 + dl];
+      }
+      __syncthreads();
+      uint32_t dtot = 0;
+      if (tid < nr) {
         for (int c = 0; c < C; ++c) {
-          const uint32_t* rt = cl.map_shared_rank(s_tot, c);
-          for (int k = 0; k < dpt; ++k) {
-            const uint32_t v = rt[d0 + k];
-            tot[k] += v;
-            if (c < cr) pre[k] += v;
-          }
+          const uint32_t v = s_tmp[c * nr + tid];
+          s_tmp[c * nr + tid] = dtot;  // exclusive prefix over CTAs
+          dtot += v;
         }
       }
-    }
-    uint32_t all;
-    uint32_t ex = block_excl_scan(tot[0] + tot[1] + tot[2] + tot[3], s_scan, &all);
-    if (d0 < ndig)
-      for (int k = 0; k < dpt; ++k) {
-        s_base[d0 + k] = ex + pre[k];
-        ex += tot[k];
+      uint32_t rtot;
+      const uint32_t dex = block_excl_scan(tid < nr ? dtot : 0u, s_scan, &rtot);
+      if (tid < nr) s_dex[tid] = dex;  // digit start within the range
+      if (tid == 0) s_rtot = rtot;
+      cl.sync();  // range totals published
+      if (tid < 32) {
+        uint32_t v = (tid < cr) ? *cl.map_shared_rank(&s_rtot, tid) : 0u;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (tid == 0) s_roff = v;
       }
-    __syncthreads();
+      __syncthreads();
+      const uint32_t roff = s_roff;
+      for (int i = tid; i < nr * C; i += CT) {
+        const int c = i / nr, dl = i % nr;
+        cl.map_shared_rank(s_base, c)[r0 + dl] = roff + s_dex[dl] + s_tmp[c * nr + dl];
+      }
+    }
+    cl.sync();  // every CTA's bases are complete
     cstamp(a.trace, 3 + 4 * p);
     // scatter into the destination CTAs' shared buffers
     const int nxt = cur ^ 1;
@@ -259,7 +260,7 @@ SortPlan make_cluster_plan(uint64_t vocab) {
 }
 
 size_t cluster_smem_bytes(int bits) {
-  return (size_t)(4 * CL_MAX_TILE + (NW + 2) * (1 << bits)) * 4;
+  return (size_t)(4 * CL_MAX_TILE + (NW + 4) * (1 << bits) + 32) * 4;
 }
 
 static int cluster_items(int K) { return K <= CL_MAX_CTAS * CL_THREADS * 4 ? 4 : 8; }
