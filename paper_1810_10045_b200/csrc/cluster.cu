@@ -133,17 +133,32 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
         s_tmp[c * nr + dl] = cl.map_shared_rank(s_tot, c)[r0 + dl];
       }
       __syncthreads();
-      uint32_t dtot = 0;
-      if (tid < nr) {
-        for (int c = 0; c < C; ++c) {
-          const uint32_t v = s_tmp[c * nr + tid];
-          s_tmp[c * nr + tid] = dtot;  // exclusive prefix over CTAs
-          dtot += v;
+      // each thread owns dpt consecutive digits of the range (nr <= 1024)
+      const int dpt = (nr + CT - 1) / CT;
+      const int dl0 = tid * dpt;
+      uint32_t dt[2] = {0u, 0u}, mysum = 0;
+      for (int k = 0; k < dpt; ++k) {
+        const int dl = dl0 + k;
+        if (dl < nr) {
+          uint32_t run = 0;
+          for (int c = 0; c < C; ++c) {
+            const uint32_t v = s_tmp[c * nr + dl];
+            s_tmp[c * nr + dl] = run;  // exclusive prefix over CTAs
+            run += v;
+          }
+          dt[k] = run;
+          mysum += run;
         }
       }
       uint32_t rtot;
-      const uint32_t dex = block_excl_scan(tid < nr ? dtot : 0u, s_scan, &rtot);
-      if (tid < nr) s_dex[tid] = dex;  // digit start within the range
+      uint32_t dex = block_excl_scan(mysum, s_scan, &rtot);
+      for (int k = 0; k < dpt; ++k) {
+        const int dl = dl0 + k;
+        if (dl < nr) {
+          s_dex[dl] = dex;  // digit start within the range
+          dex += dt[k];
+        }
+      }
       if (tid == 0) s_rtot = rtot;
       cl.sync();  // range totals published
       if (tid < 32) {
