@@ -107,6 +107,32 @@ __device__ __forceinline__ uint32_t lookback_one(uint32_t* state, uint32_t tile,
   return excl;
 }
 
+// Grid-wide barrier for a normally-launched kernel whose grid is sized to fit
+// co-resident (<= occupancy x SMs): a sense-reversing counter in global
+// memory, reused across launches (count returns to 0, gen only grows).  Avoids
+// cudaLaunchCooperativeKernel, whose launch was measured at ~15-20 us.
+struct GridBar {
+  uint32_t count;
+  uint32_t gen;
+};
+__device__ __forceinline__ void grid_barrier(GridBar* b) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
+    const uint32_t gen = ld_acquire(&b->gen);
+    __threadfence();
+    if (atomicAdd(&b->count, 1u) == nb - 1) {
+      b->count = 0u;
+      __threadfence();
+      st_release(&b->gen, gen + 1u);
+    } else {
+      while (ld_acquire(&b->gen) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // One carveout for every kernel of the library (max shared memory): the SMs
 // are then never reconfigured between the step's kernels.
 inline void max_carveout(const void* f) {

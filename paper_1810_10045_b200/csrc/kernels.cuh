@@ -7,6 +7,8 @@
 
 namespace lms {
 
+struct GridBar;
+
 // Scatter-add chunk: sorted positions per warp work item.
 constexpr int SC_CHUNK = 32;
 // Zero-row group: slots per warp work item.
@@ -114,6 +116,8 @@ struct ScatterArgs {
   int zero_rows;          // 0: every slot is present locally (world 1)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
   float lr;
+  unsigned long long* trace;
+  GridBar* bar;           // in-kernel grid barrier state (zeroed at init)
   float* M;               // U_g x D
   float* partial;         // 2 * nchunks x D
   int K;

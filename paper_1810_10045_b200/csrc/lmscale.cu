@@ -21,6 +21,7 @@
 #include <new>
 
 #include "../../include/lmscale.h"
+#include "common.cuh"
 #include "kernels.cuh"
 
 using namespace lms;
@@ -64,6 +65,7 @@ struct lmscale_ctx {
   bool m_nccl = false;
   void* m_reg = nullptr;
   NvlsState* nvls = nullptr;   // fused S5+S6 available
+  GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
   char nvls_why[256] = {0};    // why not, when it is not
   Sc1* sc1;
   Sc3* sc3;
@@ -251,6 +253,12 @@ void print_trace(lmscale_ctx* ctx, cudaStream_t s) {
   for (int i = 33; i <= 41; ++i)
     if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
   if (t[32] > t[0]) fprintf(stderr, " | S1start->S3start %.2f us", (t[32] - t[0]) * 1e-3);
+  if (t[54])
+    fprintf(stderr,
+            " | S4 cta0: phase1 %.2f (last cta done %.2f) barrier %.2f fixup %.2f (last %.2f)"
+            " | S1 end->S4 start %.2f",
+            (t[55] - t[54]) * 1e-3, (t[59] - t[54]) * 1e-3, (t[56] - t[55]) * 1e-3,
+            (t[57] - t[56]) * 1e-3, (t[61] - t[56]) * 1e-3, (t[54] - t[22]) * 1e-3);
   fprintf(stderr, "\n");
 }
 
@@ -273,6 +281,8 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.zero_rows = 1;
   a.table = nullptr;
   a.lr = 0.f;
+  a.trace = ctx->trace;
+  a.bar = ctx->bars + 0;
   a.K = (int)ctx->last_k;
   a.D = (int)ctx->cfg.dim;
   a.ug_cap = std::min<int64_t>(ctx->last_n, ctx->cfg.vocab);
@@ -374,7 +384,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_vals_b = take(4 * K), o_segidx = take(4 * K), o_inverse = take(4 * K),
            o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)), o_counts = take(4 * K),
            o_l2g = take(4 * K), o_wrank = take(4 * ctx->W), o_I = take(4 * ctx->NI),
-           o_ihat = take(4 * ctx->ucap), o_fix = take(4 * ctx->nchunks);
+           o_ihat = take(4 * ctx->ucap), o_fix = take(4 * ctx->nchunks),
+           o_bars = take(sizeof(GridBar) * 8);
     size_t o_sc3 = take(sizeof(Sc3) + sizeof(Sc1)), o_sc1 = o_sc3 + sizeof(Sc3),
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
            o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
@@ -403,6 +414,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->I = (uint32_t*)(b + o_I);
     ctx->ihat = (uint32_t*)(b + o_ihat);
     ctx->fixlist = (int32_t*)(b + o_fix);
+    ctx->bars = (GridBar*)(b + o_bars);
     ctx->sc1 = (Sc1*)(b + o_sc1);
     ctx->sc3 = (Sc3*)(b + o_sc3);
     ctx->cT = (uint32_t*)(b + o_cT);
@@ -614,6 +626,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   ctx->timing_valid = false;
   ctx->update_timed = false;
   rec(ctx, EV_FORK, s);
+  if (ctx->trace && !ctx->capturing) cudaMemsetAsync(ctx->trace, 0, 64 * sizeof(unsigned long long), s);
   const uint32_t* I = ids;
   int64_t n = k;
   if (G > 1) {

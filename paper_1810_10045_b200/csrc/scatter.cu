@@ -205,11 +205,20 @@ __device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * N
 //   phase 3  (world 1 only, after a grid barrier) S6: E[I^[r]] -= lr * M[r]
 //            -- with one rank the all-reduce is the identity, so the update
 //            rides in the same launch.
+__device__ __forceinline__ void sstamp(unsigned long long* tr, int i) {
+  if (tr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x == 0) tr[i] = t;
+    atomicMax(tr + i + 4, t);  // latest CTA
+  }
+}
+
 template <typename T, int NV, int UNR>
 __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   using V = Vec<T>;
+  sstamp(a.trace, 54);
   __shared__ T red[SC_THREADS / 32][32 * NV];
-  cg::grid_group grid = cg::this_grid();
   const int K = a.K;
   const int C = a.D / V::W;  // vectors per row
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
@@ -257,15 +266,18 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
       }
     }
   }
-  grid.sync();
+  sstamp(a.trace, 55);
+  grid_barrier(a.bar);
+  sstamp(a.trace, 56);
 
   // phase 2: runs cut by chunk boundaries
   const int nfix = (int)min(__ldcg(&a.sc1w->fixcount), (uint32_t)a.fix_cap);
   for (int64_t it = blockIdx.x; it < (int64_t)nfix * ncb; it += gridDim.x)
     fixup_item<T, NV>(a, red, __ldcg(a.fixlist + it / ncb), (int)(it % ncb), C);
+  sstamp(a.trace, 57);
 
   if (!a.table) return;
-  grid.sync();
+  grid_barrier(a.bar);
 
   // phase 3 (world 1): S6 row update, warp per row
   T* E = reinterpret_cast<T*>(a.table);
@@ -314,10 +326,10 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   const int64_t cap = (int64_t)a.num_sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phases 2/3 want a wide grid
-  ScatterArgs args = a;
-  void* kargs[] = {(void*)&args};
-  return cudaLaunchCooperativeKernel((void*)k_scatter<T, NV, UNR>, dim3((unsigned)blocks),
-                                     dim3(SC_THREADS), kargs, 0, s);
+  // grid <= occupancy x SMs: every CTA is co-resident, so the in-kernel
+  // grid barrier is safe with a normal launch
+  k_scatter<T, NV, UNR><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
