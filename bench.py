@@ -222,7 +222,7 @@ def main():
     lr = synth.default_lr(args.mode)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
-    flags = lmscale.FLAG_TIMING | (0 if args.no_graph else lmscale.FLAG_GRAPH)
+    flags = 0 if args.no_graph else lmscale.FLAG_GRAPH
     if world > 1:
         ctx = make_context(cfg.V, cfg.K, cfg.D, flags=flags)
     else:
@@ -268,14 +268,25 @@ def main():
 
     clk = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
                  if "CUDA_VISIBLE_DEVICES" in os.environ else local)
+    # Timed region: only the two events that bracket the S4 kernel are
+    # recorded inside the step (each event node costs ~3 us of GPU time).
+    ctx.set_timing(1)
+    scat = []
+
+    def collect_s4():
+        scat.append(ctx.stats()["us_scatter"])
     clk.start()
     for _ in range(args.warmup):
         step()
     k_before = ctx.stats()["kernels_total_lo"]
-    ms = timed(step, args.steps, 0, collect)
+    ms = timed(step, args.steps, 0, collect_s4)
     launches[0] = ctx.stats()["kernels_total_lo"] - k_before
     clocks = clk.stop()
     info["ug"] = ctx.sparse_grad().num_unique
+    # Diagnostic pass (not timed for `value`): every phase bracketed by events.
+    ctx.set_timing(2)
+    timed(step, 3, 1, collect)
+    ctx.set_timing(0)
     total_ms = max_over_ranks(sum(ms), dev)
     ms_step = total_ms / args.steps
     tokens = world * cfg.K
@@ -285,12 +296,14 @@ def main():
 
     # per-phase device times (median over timed steps), max over ranks
     ph = {k: max_over_ranks(statistics.median(v), dev) for k, v in phase.items() if v}
+    ph["note"] = "diagnostic pass with an event around every phase (~3 us each); not the timed region"
+    s4_us = max_over_ranks(statistics.median(scat), dev)
     hbm_peak, peak_kind = peaks()
     st_last = ctx.stats()
     D = cfg.D
     kname = "k_scatter (S4 segmented scatter-add + cut-run fixup, one cooperative launch)"
     scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
-    scatter_us = ph["us_scatter"]
+    scatter_us = s4_us
     roof = {"kernel": kname, "bound": "hbm",
             "achieved": scatter_bytes / (scatter_us * 1e-6) / 1e9, "peak": hbm_peak,
             "unit": "GB/s", "peak_kind": peak_kind,
@@ -362,7 +375,7 @@ def main():
                 "counter-hash fp32 gradients/table; no datasets)",
                 "config": config_dict(cfg, args, world),
                 "U_local": info.get("u_local"), "U_global": ug, "E_U_global_closed_form": eu,
-                "phases_us_median": ph, "roofline": roof, "roofline_s5_s6": upd,
+                "phases_us_diagnostic": ph, "roofline": roof, "roofline_s5_s6": upd,
                 "dense_baseline": dense, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": sync_launches, "gpu_launches_per_step": sync_launches / args.steps,
                 "library": lmscale.version()}

@@ -234,6 +234,12 @@ LMSCALE_API lmscale_status lmscale_train_step_host(lmscale_ctx* ctx, const uint3
 
 /* ---------------------------------------------------------------- misc */
 
+/* Timing mode of subsequent calls: 0 none, 1 only the two events bracketing
+ * the S4 kernel (us_scatter), 2 every phase (all us_* fields; each event is a
+ * GPU-side serialisation point of a few microseconds, so mode 2 inflates the
+ * step it measures).  FLAG_TIMING at init selects mode 2. */
+LMSCALE_API lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode);
+
 LMSCALE_API lmscale_status lmscale_get_stats(const lmscale_ctx* ctx, lmscale_stats* out /* host */);
 LMSCALE_API const char* lmscale_status_string(lmscale_status s);
 /* Last detailed error message of this context (static storage inside ctx). */

@@ -263,6 +263,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   }
   cstamp(a.trace, 22);
   cl.sync();  // no CTA leaves while another may still read its shared memory
+  if (a.trace && threadIdx.x == 0) {  // latest exit over all CTAs
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(a.trace + 62, t);
+  }
 }
 
 SortPlan make_cluster_plan(uint64_t vocab) {

@@ -100,6 +100,7 @@ struct lmscale_ctx {
   int kernels_call = 0;
   int64_t kernels_total = 0;
   char err[512] = {0};
+  int tmode = 0;                        // timing mode, see rec()
   unsigned long long* trace = nullptr;  // LMSCALE_PHASE_TRACE diagnostics (64 stamps)
 };
 
@@ -147,10 +148,14 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 bool comm_enabled(const lmscale_ctx* c) {
   return c->cfg.world > 1 && !(c->cfg.flags & LMSCALE_FLAG_NO_COMM);
 }
-bool timing(const lmscale_ctx* c) { return (c->cfg.flags & LMSCALE_FLAG_TIMING) != 0; }
+bool timing(const lmscale_ctx* c) { return c->tmode != 0; }
 
+// Timing modes (lmscale_set_timing): 0 none, 1 only the two events that
+// bracket the S4 kernel, 2 every phase.  Each event is a GPU-side
+// serialisation point (~3 us measured), so mode 1 is the one to time steps in.
 void rec(lmscale_ctx* c, int ev, cudaStream_t s) {
-  if (!timing(c)) return;
+  if (c->tmode == 0) return;
+  if (c->tmode == 1 && ev != EV_S3_END && ev != EV_SCATTER_END) return;
   if (c->capturing)  // a timing node inside the CUDA graph
     cudaEventRecordWithFlags(c->tev[ev], s, cudaEventRecordExternal);
   else
@@ -259,6 +264,9 @@ void print_trace(lmscale_ctx* ctx, cudaStream_t s) {
             " | S1 end->S4 start %.2f",
             (t[55] - t[54]) * 1e-3, (t[59] - t[54]) * 1e-3, (t[56] - t[55]) * 1e-3,
             (t[57] - t[56]) * 1e-3, (t[61] - t[56]) * 1e-3, (t[54] - t[22]) * 1e-3);
+  if (t[62] && t[63])
+    fprintf(stderr, " | S1 cta0 last stamp -> S1 last exit %.2f, S1 last exit -> S4 first start %.2f",
+            (t[62] - t[22]) * 1e-3, ((long long)(~t[63]) - (long long)t[62]) * 1e-3);
   fprintf(stderr, "\n");
 }
 
@@ -338,6 +346,17 @@ const char* lmscale_status_string(lmscale_status s) {
 }
 
 const char* lmscale_last_error(const lmscale_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 2) return LMSCALE_ERR_INVALID_ARG;
+  if (mode != ctx->tmode && ctx->gexec) {  // the captured graph carries the old events
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  ctx->tmode = mode;
+  ctx->timing_valid = false;
+  return LMSCALE_OK;
+}
 
 lmscale_status lmscale_get_nccl_id(uint8_t out_id[128]) {
   if (!out_id) return LMSCALE_ERR_INVALID_ARG;
@@ -434,8 +453,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&ctx->s_cap, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
-    if (timing(ctx))
-      for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&ctx->tev[i]));
+    for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&ctx->tev[i]));
+    ctx->tmode = (cfg->flags & LMSCALE_FLAG_TIMING) ? 2 : 0;
     if (comm_enabled(ctx)) {
       if (!nccl_id) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "world > 1 needs an NCCL id");
       ncclUniqueId id;
@@ -839,7 +858,9 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
       ctx->kernels_total -= ctx->kernels_call;  // captured, not launched yet
     }
     begin_call(ctx);
+    if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * sizeof(unsigned long long), s));
     CK(cudaGraphLaunch(ctx->gexec, s));
+    print_trace(ctx, s);
     ctx->kernels_call = ctx->gkey.kernels;
     ctx->fused_last = ctx->gkey.fused;
     ctx->timing_valid = timing(ctx);
@@ -958,7 +979,12 @@ lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
   if (!cctx || !out) return LMSCALE_ERR_INVALID_ARG;
   lmscale_ctx* ctx = const_cast<lmscale_ctx*>(cctx);
   lmscale_stats& st = ctx->stats;
-  if (ctx->timing_valid) {
+  st.us_dedup = st.us_gather = st.us_merge = st.us_scatter = st.us_allreduce = st.us_update =
+      st.us_total = -1.0;
+  if (ctx->timing_valid && ctx->tmode == 1) {
+    CK(cudaEventSynchronize(ctx->tev[EV_SCATTER_END]));
+    st.us_scatter = 1e3 * ev_ms(ctx, EV_S3_END, EV_SCATTER_END);
+  } else if (ctx->timing_valid && ctx->tmode == 2) {
     CK(cudaEventSynchronize(ctx->tev[EV_AR_END]));
     if (ctx->update_timed) CK(cudaEventSynchronize(ctx->tev[EV_UPD_END]));
     st.us_dedup = 1e3 * ev_ms(ctx, EV_S1_BEGIN, EV_S1_END);

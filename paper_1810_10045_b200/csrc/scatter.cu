@@ -218,6 +218,11 @@ template <typename T, int NV, int UNR>
 __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   using V = Vec<T>;
   sstamp(a.trace, 54);
+  if (a.trace && threadIdx.x == 0) {  // earliest start over all CTAs (as ~t)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(a.trace + 63, ~t);
+  }
   __shared__ T red[SC_THREADS / 32][32 * NV];
   const int K = a.K;
   const int C = a.D / V::W;  // vectors per row

@@ -80,6 +80,7 @@ _dense = _sig("lmscale_sync_dense_baseline", _S, [_P, _P, _P, _i64, _P, ctypes.c
 _dense_apply = _sig("lmscale_dense_apply", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, _P])
 _host_step = _sig("lmscale_train_step_host", _S,
                   [_P, _P, _P, _i64, _P, ctypes.c_float, _P, ctypes.POINTER(_i64), _P])
+_set_timing = _sig("lmscale_set_timing", _S, [_P, ctypes.c_int])
 _get_stats = _sig("lmscale_get_stats", _S, [_P, ctypes.POINTER(StatsC)])
 _status_string = _sig("lmscale_status_string", ctypes.c_char_p, [_S])
 _last_error = _sig("lmscale_last_error", ctypes.c_char_p, [_P])
@@ -89,7 +90,8 @@ EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_u
             "lmscale_global_unique", "lmscale_scatter_expand", "lmscale_get_sparse_grad",
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
             "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
-            "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_get_stats",
+            "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing",
+            "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
 
 
@@ -297,6 +299,10 @@ class Context:
                                _ptr(table), float(lr), _ptr(ids_out_host), ctypes.byref(n),
                                _stream(stream)), "lmscale_train_step_host")
         return int(n.value)
+
+    def set_timing(self, mode: int):
+        """0 none, 1 S4-only events, 2 every phase (see lmscale_set_timing)."""
+        self._check(_set_timing(self._h, int(mode)), "lmscale_set_timing")
 
     def stats(self) -> dict:
         s = StatsC()

@@ -8,7 +8,7 @@ for f in sys.argv[1:]:
         if not line.startswith("{"):
             continue
         d = json.loads(line)
-        ph = {k.replace("us_", ""): round(v, 1) for k, v in (d.get("phases_us_median") or {}).items()}
+        ph = {k.replace("us_", ""): round(v, 1) for k, v in (d.get("phases_us_median") or d.get("phases_us_diagnostic") or {}).items() if k != "note"}
         dn = d.get("dense_baseline") or {}
         print(f"{f}: {d['config']['workload']} N={d['n_gpus']} {d['value']/1e6:.1f} Mtok/s "
               f"{d.get('us_per_step', 0):.1f} us/step U_g={d.get('U_global')} phases={ph} "

@@ -33,7 +33,9 @@ if world > 1:
     table = synth.table_values(cfg.V, cfg.D, "signed", device=dev)
     ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
 else:
-    ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+    flags = (0 if os.environ.get("TRACE_NO_EVENTS") else lmscale.FLAG_TIMING) | \
+        (lmscale.FLAG_GRAPH if os.environ.get("TRACE_GRAPH") else 0)
+    ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, flags=flags)
 for i in range(steps):
     ctx.step(ids, grad, table, 0.1)
     torch.cuda.synchronize()
