@@ -218,7 +218,6 @@ def main():
     J = synth.ids_for(cfg, rank)
     ids = torch.from_numpy(J.view(np.int32)).to(dev)
     grad = synth.grad_values(cfg.K, cfg.D, args.mode, rank=rank, device=dev)
-    table = synth.table_values(cfg.V, cfg.D, args.mode, device=dev)
     lr = synth.default_lr(args.mode)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
@@ -227,6 +226,14 @@ def main():
         ctx = make_context(cfg.V, cfg.K, cfg.D, flags=flags)
     else:
         ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, device=local, flags=flags)
+    # the table: with G > 1 the context allocates it in a symmetric window so
+    # the fused S5+S6 kernel multicasts updated rows into every replica
+    if world > 1:
+        table = ctx.alloc_table()
+        table.copy_(synth.table_values(cfg.V, cfg.D, args.mode, device=dev))
+    else:
+        table = synth.table_values(cfg.V, cfg.D, args.mode, device=dev)
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 
     def barrier():

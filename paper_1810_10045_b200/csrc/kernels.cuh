@@ -143,8 +143,12 @@ struct NvlsState;
 NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char* err,
                        size_t errlen);
 void nvls_destroy(ncclComm_t comm, NvlsState* st);
+// twin != nullptr: `table` is the symmetric-window table registered as twin.
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
-                        unsigned long long* trace, cudaStream_t s);
+                        unsigned long long* trace, ncclWindow_t twin, cudaStream_t s);
+ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,
+                                 size_t errlen);
+void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w);
 
 }  // namespace lms

@@ -66,6 +66,10 @@ struct lmscale_ctx {
   void* m_reg = nullptr;
   NvlsState* nvls = nullptr;   // fused S5+S6 available
   GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
+  float* table_ptr = nullptr;  // lmscale_alloc_table
+  size_t table_bytes = 0;
+  bool table_nccl = false;
+  ncclWindow_t table_win = nullptr;  // symmetric window of the table (NVLS direct update)
   char nvls_why[256] = {0};    // why not, when it is not
   Sc1* sc1;
   Sc3* sc3;
@@ -83,7 +87,7 @@ struct lmscale_ctx {
   const int32_t* sorted_vals = nullptr;
   int64_t last_ug = 0;
   bool have_pending_ug = false;  // last step did not read U_g back to the host
-  bool fused_last = false;       // last step used the fused NVLS S5+S6 kernel
+  int fused_last = 0;  // last step used the fused NVLS S5+S6 kernel (2: direct into E windows)
   // CUDA graph of lmscale_step (LMSCALE_FLAG_GRAPH)
   bool capturing = false;
   cudaStream_t s_cap = nullptr;
@@ -94,7 +98,7 @@ struct lmscale_ctx {
     int64_t k;
     float lr;
     int kernels;
-    bool fused;
+    int fused;
   } gkey{};
   lmscale_stats stats{};
   int kernels_call = 0;
@@ -347,6 +351,34 @@ const char* lmscale_status_string(lmscale_status s) {
 
 const char* lmscale_last_error(const lmscale_ctx* ctx) { return ctx ? ctx->err : "null context"; }
 
+lmscale_status lmscale_alloc_table(lmscale_ctx* ctx, float** table_out, int64_t* bytes_out) {
+  if (!ctx || !table_out) return LMSCALE_ERR_INVALID_ARG;
+  if (ctx->table_ptr) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "table already allocated");
+  const size_t bytes = 4 * (size_t)ctx->cfg.vocab * ctx->cfg.dim;
+  if (ctx->nvls) {
+    const size_t al = ((bytes + (1 << 21) - 1) >> 21) << 21;
+    void* p = nullptr;
+    if (ncclMemAlloc(&p, al) != ncclSuccess)
+      return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(table, %zu)", al);
+    ctx->table_ptr = (float*)p;
+    ctx->table_nccl = true;
+    ctx->table_bytes = al;
+    char why[256] = {0};
+    ctx->table_win = nvls_register_table(ctx->comm, p, al, why, sizeof(why));
+    if (!ctx->table_win) snprintf(ctx->nvls_why, sizeof(ctx->nvls_why), "%s", why);
+  } else {
+    if (cudaMalloc((void**)&ctx->table_ptr, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->table_ptr = nullptr;
+      return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(table, %zu)", bytes);
+    }
+    ctx->table_bytes = bytes;
+  }
+  *table_out = ctx->table_ptr;
+  if (bytes_out) *bytes_out = (int64_t)bytes;
+  return LMSCALE_OK;
+}
+
 lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return LMSCALE_ERR_INVALID_ARG;
   if (mode != ctx->tmode && ctx->gexec) {  // the captured graph carries the old events
@@ -506,6 +538,13 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
+  if (ctx->table_ptr) {
+    if (ctx->table_win) nvls_deregister_table(ctx->comm, ctx->table_win);
+    if (ctx->table_nccl)
+      ncclMemFree(ctx->table_ptr);
+    else
+      cudaFree(ctx->table_ptr);
+  }
   if (ctx->nvls) nvls_destroy(ctx->comm, ctx->nvls);
   if (ctx->m_reg) ncclCommDeregister(ctx->comm, ctx->m_reg);
   if (ctx->M) {
@@ -698,7 +737,8 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   if (G > 1 && table && ctx->nvls) {
     // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
-                       ctx->cfg.rank, G, ctx->trace, s);
+                       ctx->cfg.rank, G, ctx->trace,
+                       table == ctx->table_ptr ? ctx->table_win : nullptr, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {
@@ -715,7 +755,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
-    ctx->fused_last = true;
+    ctx->fused_last = (table == ctx->table_ptr && ctx->table_win) ? 2 : 1;
     int64_t ug = -1;
     if (need_host_ug) {
       CK(cudaEventSynchronize(ctx->ev_copy));
@@ -736,7 +776,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     end_call(ctx);
     return LMSCALE_OK;
   }
-  ctx->fused_last = false;
+  ctx->fused_last = 0;
   if (G == 1 && table && !need_host_ug) {
     // S6 straight away with the device-side count: no host round trip.
     rec(ctx, EV_AR_END, s);
@@ -995,7 +1035,7 @@ lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
     st.us_update = ctx->update_timed ? 1e3 * ev_ms(ctx, EV_UPD_BEGIN, EV_UPD_END) : -1.0;
     st.us_total = 1e3 * ev_ms(ctx, EV_FORK, ctx->update_timed ? EV_UPD_END : EV_AR_END);
   }
-  st.fused_s5_s6 = ctx->fused_last ? 1 : 0;
+  st.fused_s5_s6 = ctx->fused_last;
   st.nvls_available = ctx->nvls ? 1 : 0;
   *out = st;
   return LMSCALE_OK;

@@ -73,6 +73,8 @@ struct NvlsKernelArgs {
   int rank, world;
   unsigned long long* trace;
   int diag;  // timing diagnostics only (LMSCALE_NVLS_DIAG): 1 no broadcast, 2 no reduce
+  ncclWindow_t twin;  // non-null: the table is in a symmetric window; updated rows are
+                      // multicast straight into every replica of E (no copy phase)
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -100,6 +102,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
   const int64_t nw = (int64_t)gridDim.x * NV_WARPS;
   T* mc = reinterpret_cast<T*>(ncclGetLsaMultimemPointer(a.win, 0, a.dev));
   T* E = reinterpret_cast<T*>(a.table);
+  T* mcE = a.twin ? reinterpret_cast<T*>(ncclGetLsaMultimemPointer(a.twin, 0, a.dev)) : nullptr;
   const T* Ml = reinterpret_cast<const T*>(a.M);
 
   // owned rows r = rank + G*t (interleaved over the id space, so every rank
@@ -108,8 +111,10 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
   {
     for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
       const int64_t r = a.rank + a.world * t;
-      T* er = E + (size_t)__ldg(a.ihat + r) * C;
+      const size_t wrow = (size_t)__ldg(a.ihat + r) * C;
+      T* er = E + wrow;
       T* mr = mc + (size_t)r * C;
+      T* dst = mcE ? mcE + wrow : mr;  // multicast target: E replicas, or M
       int c = lane;
       // 8 independent multicast reductions (+ 8 local E loads) in flight per lane
       for (; c + 224 < C; c += 256) {
@@ -126,23 +131,27 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           e[q] = fma4(-a.lr, m[q], e[q]);
-          er[c + 32 * q] = e[q];
+          if (!mcE) er[c + 32 * q] = e[q];
         }
         if (a.diag != 1) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) mm_st(mr + c + 32 * q, e[q]);
+          for (int q = 0; q < 8; ++q) mm_st(dst + c + 32 * q, e[q]);
         }
       }
       for (; c < C; c += 32) {
         const T e = fma4(-a.lr, mm_ld_reduce(mr + c), er[c]);
-        er[c] = e;
-        mm_st(mr + c, e);
+        if (!mcE) er[c] = e;
+        mm_st(dst + c, e);
       }
     }
   }
   nv_stamp(a.trace, 50);
   bar.sync(cta, cuda::memory_order_acq_rel);  // the other ranks' rows have landed
   nv_stamp(a.trace, 51);
+  if (mcE) {  // every replica already holds every updated row
+    nv_stamp(a.trace, 52);
+    return;
+  }
 
   // rows owned by the other ranks: copy the broadcast result into E
   for (int j = 0; j < a.world; ++j) {
@@ -214,10 +223,26 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st) {
   delete st;
 }
 
+ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,
+                                 size_t errlen) {
+  ncclWindow_t w = nullptr;
+  ncclResult_t r = ncclCommWindowRegister(comm, table, bytes, &w, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    snprintf(err, errlen, "ncclCommWindowRegister(table): %s", ncclGetErrorString(r));
+    return nullptr;
+  }
+  return w;
+}
+
+void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w) {
+  if (w) ncclCommWindowDeregister(comm, w);
+}
+
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
-                        unsigned long long* trace, cudaStream_t s) {
+                        unsigned long long* trace, ncclWindow_t twin, cudaStream_t s) {
   NvlsKernelArgs a;
+  a.twin = twin;
   a.trace = trace;
   static const int diag = getenv("LMSCALE_NVLS_DIAG") ? atoi(getenv("LMSCALE_NVLS_DIAG")) : 0;
   a.diag = diag;

@@ -80,6 +80,7 @@ _dense = _sig("lmscale_sync_dense_baseline", _S, [_P, _P, _P, _i64, _P, ctypes.c
 _dense_apply = _sig("lmscale_dense_apply", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, _P])
 _host_step = _sig("lmscale_train_step_host", _S,
                   [_P, _P, _P, _i64, _P, ctypes.c_float, _P, ctypes.POINTER(_i64), _P])
+_alloc_table = _sig("lmscale_alloc_table", _S, [_P, ctypes.POINTER(_P), ctypes.POINTER(_i64)])
 _set_timing = _sig("lmscale_set_timing", _S, [_P, ctypes.c_int])
 _get_stats = _sig("lmscale_get_stats", _S, [_P, ctypes.POINTER(StatsC)])
 _status_string = _sig("lmscale_status_string", ctypes.c_char_p, [_S])
@@ -90,7 +91,7 @@ EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_u
             "lmscale_global_unique", "lmscale_scatter_expand", "lmscale_get_sparse_grad",
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
             "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
-            "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing",
+            "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing", "lmscale_alloc_table",
             "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
 
@@ -299,6 +300,14 @@ class Context:
                                _ptr(table), float(lr), _ptr(ids_out_host), ctypes.byref(n),
                                _stream(stream)), "lmscale_train_step_host")
         return int(n.value)
+
+    def alloc_table(self) -> torch.Tensor:
+        """The context-owned vocab x dim table (lmscale_alloc_table): with world > 1
+        and NVLS it is a symmetric window and updates are multicast into every
+        replica.  Collective when world > 1.  Returns a zero-copy float32 view."""
+        p, n = _P(), _i64()
+        self._check(_alloc_table(self._h, ctypes.byref(p), ctypes.byref(n)), "lmscale_alloc_table")
+        return _view(p.value, (int(self.cfg.vocab), self.dim), torch.float32, self.device)
 
     def set_timing(self, mode: int):
         """0 none, 1 S4-only events, 2 every phase (see lmscale_set_timing)."""

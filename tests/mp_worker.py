@@ -79,7 +79,7 @@ def run_small(ctx_full, cfg, mode, rank, G, dev):
     ctx.close()
 
 
-def run_fused_small(cfg, mode, rank, G, dev):
+def run_fused_small(cfg, mode, rank, G, dev, own_table=False):
     """lmscale_step (S1-S6 in one call; S5+S6 as the fused NVLS kernel when the
     box has multicast) against the oracle; replicas must be bit-identical."""
     lr = synth.default_lr(mode)
@@ -87,13 +87,18 @@ def run_fused_small(cfg, mode, rank, G, dev):
     Dh = [synth.grad_values(cfg.K, cfg.D, mode, rank=g) for g in range(G)]
     E0 = synth.table_values(cfg.V, cfg.D, mode)
     ctx = make_context(cfg.V, cfg.K, cfg.D)
-    E = E0.to(dev)
+    if own_table:   # the context's symmetric-window table (direct multicast update)
+        E = ctx.alloc_table()
+        E.copy_(E0.to(dev))
+        torch.cuda.synchronize()
+    else:
+        E = E0.to(dev)
     ug = ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), E, lr,
                   want_num_unique=True)
     torch.cuda.synchronize()
     st = ctx.stats()
     if os.environ.get("LMSCALE_REQUIRE_NVLS") == "1":
-        assert st["fused_s5_s6"] == 1, "fused NVLS path did not run"
+        assert st["fused_s5_s6"] == (2 if own_table else 1), f"fused NVLS path: {st['fused_s5_s6']}"
     Eo = E0.numpy().copy()
     ref = oracle.sync_unique(J, [d.numpy() for d in Dh], Eo, lr)
     assert ug == ref["Ug"]
@@ -114,8 +119,8 @@ def run_fused_small(cfg, mode, rank, G, dev):
     torch.cuda.synchronize()
     check_replicas(E, f"fused step 2 {cfg.name} {mode}")
     if rank == 0:
-        print(f"fused={st['fused_s5_s6']} nvls={st['nvls_available']} G={G} {cfg.name} {mode}",
-              flush=True)
+        print(f"fused={st['fused_s5_s6']} nvls={st['nvls_available']} G={G} {cfg.name} {mode} "
+              f"own_table={own_table}", flush=True)
     ctx.close()
 
 
@@ -176,6 +181,8 @@ def main():
         for mode in ("int", "signed"):
             run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev)
         run_fused_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
+        for mode in ("int", "signed"):
+            run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev, own_table=True)
     for name in ("1b", "char", "amazon", "tieba"):
         if name in which:
             run_full(synth.CONFIGS[name], rank, G, dev)
