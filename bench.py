@@ -248,6 +248,8 @@ def main():
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(steps)]
         for i in range(steps):
+            if world > 1:
+                dist.barrier()     # ranks enter each timed step together (outside the events)
             flush.zero_()
             ev[i][0].record(stream)
             fn()
