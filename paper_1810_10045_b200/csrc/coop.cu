@@ -110,7 +110,6 @@ __device__ __forceinline__ void warp_offsets(uint32_t* s_cnt, int ndig, uint32_t
 __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
   extern __shared__ uint32_t smem[];
   __shared__ uint32_t s_scan[32];
-  cg::grid_group grid = cg::this_grid();
   const int ndig = 1 << a.bits;
   uint32_t* s_cnt = smem;                 // [NW][ndig]
   uint32_t* s_base = smem + NW * ndig;    // [ndig]
@@ -156,7 +155,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
       __syncthreads();
     }
     stamp(a.trace, 1 + 4 * p);
-    grid.sync();
+    grid_barrier(a.bar);
     stamp(a.trace, 2 + 4 * p);
     // P2: bases from the digit-major count rows, then the stable scatter
     for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
       __syncthreads();
     }
     stamp(a.trace, 3 + 4 * p);
-    grid.sync();
+    grid_barrier(a.bar);
     stamp(a.trace, 4 + 4 * p);
     kin = kout;
     vin = vout;
@@ -241,7 +240,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
     if (tid == 0) a.heads[t] = tot;
   }
   stamp(a.trace, 20);
-  grid.sync();
+  grid_barrier(a.bar);
   stamp(a.trace, 21);
   for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
     if (!single) load_sorted(t);
@@ -292,7 +291,6 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
 
 __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   __shared__ uint32_t s_scan[32];
-  cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t gtid = (int64_t)blockIdx.x * CT + tid;
   const int64_t gthreads = (int64_t)gridDim.x * CT;
@@ -305,7 +303,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
     a.sc->u_global = 0;
   }
   stamp(a.trace, 33);
-  grid.sync();
+  grid_barrier(a.bar);
   stamp(a.trace, 34);
 
   // phase A: presence bits.  Words < CO_HOTW (the head of a frequency-ordered
@@ -351,7 +349,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   }
   if (bad) atomicOr(&a.sc->err, 1u);
   stamp(a.trace, 35);
-  grid.sync();
+  grid_barrier(a.bar);
   stamp(a.trace, 36);
 
   // phase B: popcounts of this CTA's word range (one word per thread per round)
@@ -363,7 +361,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   const uint32_t cta_tot = block_sum(cnt, s_scan);
   if (tid == 0) a.ctot[blockIdx.x] = cta_tot;
   stamp(a.trace, 37);
-  grid.sync();
+  grid_barrier(a.bar);
   stamp(a.trace, 38);
 
   // phase C: CTA prefix, per-word ranks, ascending I^ emission.  Emission is
@@ -389,7 +387,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   }
   stamp(a.trace, 39);
   if (!a.luniq) return;
-  grid.sync();
+  grid_barrier(a.bar);
   stamp(a.trace, 40);
 
   // phase D: l2g[u] = slot of J^[u] in I^ (S1 of this rank has completed)
@@ -465,9 +463,9 @@ int coop_grid_s1(int ntiles, int num_sms) {
 
 cudaError_t launch_s1(const S1Args& a, int num_sms, cudaStream_t s) {
   const int grid = coop_grid_s1(a.ntiles, num_sms);
-  void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((void*)k_s1, dim3(grid), dim3(CO_THREADS), args,
-                                     s1_smem_bytes(a.bits), s);
+  // grid <= co-resident capacity: the in-kernel barrier is safe with a normal launch
+  k_s1<<<grid, CO_THREADS, s1_smem_bytes(a.bits), s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s) {
@@ -485,8 +483,8 @@ cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s) {
   if (want < 1) want = 1;
   const int64_t cap = (int64_t)num_sms * occ;
   const int grid = (int)(want < cap ? want : cap);
-  void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((void*)k_s3, dim3(grid), dim3(CO_THREADS), args, 0, s);
+  k_s3<<<grid, CO_THREADS, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace lms

@@ -63,6 +63,7 @@ struct S1Args {
   uint32_t* ihat;
   int32_t* l2g;
   Sc3* sc3;
+  GridBar* bar;  // in-kernel grid barrier (cooperative-size grid, normal launch)
 };
 struct S3Args {
   const uint32_t* I;
@@ -78,6 +79,7 @@ struct S3Args {
   const Sc1* sc1;
   int32_t* l2g;
   unsigned long long* trace;
+  GridBar* bar;
 };
 SortPlan make_coop_plan(uint64_t vocab);
 

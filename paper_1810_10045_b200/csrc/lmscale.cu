@@ -205,6 +205,7 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   a.sc = ctx->sc1;
   a.nu_out = nu_out;
   a.trace = ctx->trace;
+  a.bar = ctx->bars + 1;
   if (!getenv("LMSCALE_NO_CLUSTER") && cluster_s1_ok((int)k)) {
     // small K: the whole sort in one thread-block cluster (DSMEM)
     a.passes = ctx->cl_plan.passes;
@@ -243,6 +244,7 @@ lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream
   a.sc1 = ctx->sc1;
   a.l2g = ctx->l2g;
   a.trace = ctx->trace;
+  a.bar = ctx->bars + 2;
   CK(launch_s3(a, ctx->num_sms, s));
   LAUNCHED(1);
   ctx->last_n = n;
