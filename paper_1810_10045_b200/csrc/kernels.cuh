@@ -11,9 +11,8 @@ struct GridBar;
 
 // Scatter-add chunk: sorted positions per warp work item.
 constexpr int SC_CHUNK = 32;
-// Chunks per CTA work item (one per warp); partial rows exist only at the
-// edges of these 256-position groups.
-constexpr int SC_GROUP = 8;
+// Zero-row group: slots per warp work item.
+constexpr int SC_ZGROUP = 32;
 
 // Per-step device scalars of S1 (zeroed at the start of S1).
 struct Sc1 {
@@ -114,7 +113,7 @@ struct ScatterArgs {
   const Sc3* sc3;         // U_g
   const Sc1* sc1;         // U_i
   Sc1* sc1w;              // fixup list counter
-  int32_t* fixlist;       // owner groups of cut runs
+  int32_t* fixlist;       // owner chunks of cut runs
   int fix_cap;
   int zero_rows;          // 0: every slot is present locally (world 1)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
@@ -122,7 +121,7 @@ struct ScatterArgs {
   unsigned long long* trace;
   GridBar* bar;           // in-kernel grid barrier state (zeroed at init)
   float* M;               // U_g x D
-  float* partial;         // 2 * ngroups x D
+  float* partial;         // 2 * nchunks x D
   int K;
   int D;
   int64_t ug_cap;         // capacity bound on U_g (sizes the grid)

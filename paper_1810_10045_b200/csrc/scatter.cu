@@ -58,25 +58,13 @@ constexpr unsigned FULL_MASK = 0xffffffffu;
 }  // namespace
 
 // ------------------------------------------------------------------- S4
-//
-// Work item = (group of SC_GROUP = 8 consecutive 32-position chunks, column
-// block); one CTA per item, warp w takes chunk 8g + w.  Each warp sums the
-// runs of its chunk in registers: runs inside the chunk go straight to M;
-// the run cut by the chunk's left edge (head piece) and the one cut by its
-// right edge (tail piece) go to shared memory.  Warp 0 then merges the
-// group's pieces in order: a run that ends inside the group is stored once to
-// M, a run cut by the GROUP's edges becomes a global partial row (head P[2g],
-// tail P[2g+1]) and the group holding its start appends itself to the fix-up
-// list.  Only group edges produce global partials (8x fewer than chunk
-// edges), so the fix-up phase of a 33K-row Zipf head run is small.
 
-// One chunk [i0, i0 + n) for one column block.  FULL: n == SC_CHUNK and the
-// column block lies inside the row (no predicates).
+// One chunk of sorted positions [i0, i0 + n) for one column block.  FULL:
+// n == SC_CHUNK and the column block lies inside the row (no predicates).
 template <typename T, int NV, int UNR, bool FULL>
 __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __restrict__ g,
-                                              T* __restrict__ M, int c, int n, int col0, int C,
-                                              int lane, T* __restrict__ sH, T* __restrict__ sT,
-                                              int* hu, int* tu) {
+                                              T* __restrict__ M, T* __restrict__ P, int c,
+                                              int n, int col0, int C, int lane) {
   using V = Vec<T>;
   const int K = a.K;
   const int i0 = c * SC_CHUNK;
@@ -91,10 +79,8 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   if (FULL || lane < n) my_slot = a.zero_rows ? __ldg(a.l2g + my_u) : my_u;
   const int up = __shfl_up_sync(FULL_MASK, my_u, 1);
   const unsigned hmask = __ballot_sync(FULL_MASK, (FULL || lane < n) && (lane == 0 || my_u != up));
-  const int u_first = __shfl_sync(FULL_MASK, my_u, 0);
-  const int u_last = __shfl_sync(FULL_MASK, my_u, n - 1);
-  const bool split_left = u_first == prev_u;
-  const bool split_right = u_last == next_u;
+  const bool split_left = __shfl_sync(FULL_MASK, my_u, 0) == prev_u;
+  const bool split_right = __shfl_sync(FULL_MASK, my_u, n - 1) == next_u;
   T acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = V::zero();
@@ -128,19 +114,23 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
           const int slot = __shfl_sync(FULL_MASK, my_slot, p);
           T* dst;
           if (seg_first && split_left) {
-            dst = sH;
-            if (lane == 0) *hu = u_first;
+            dst = P + (size_t)(2 * c) * C;
           } else if (last && split_right) {
-            dst = sT;
-            if (lane == 0) *tu = u_last;
+            dst = P + (size_t)(2 * c + 1) * C;
+            // this chunk holds the start of a run cut by its end: it owns the
+            // run's fixup (listed once, by column block 0)
+            if (col0 == lane && lane == 0) {
+              const uint32_t idx = atomicAdd(&a.sc1w->fixcount, 1u);
+              if (idx < (uint32_t)a.fix_cap) a.fixlist[idx] = c;
+            }
           } else {
-            dst = slot >= 0 ? M + (size_t)slot * C + col0 - lane : nullptr;
+            dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
           }
           if (dst) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
               const int col = col0 + v * 32;
-              if (FULL || col < C) V::st(dst + lane + v * 32, acc[v]);
+              if (FULL || col < C) V::st(dst + col, acc[v]);
             }
           }
 #pragma unroll
@@ -152,25 +142,24 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   }
 }
 
-// Phase 2 (fixup) for one (owner group g, column block): sum the run's
-// partials P[2g+1] (tail of g) and P[2g'] (heads of g < g' <= g1) in a fixed
+// Phase 2 (fixup) for one (owner chunk c, column block): sum the run's
+// partials P[2c+1] (tail of c) and P[2c'] (heads of c < c' <= c1) in a fixed
 // order -- warp w sums partials w, w+8, ...; warps are combined in warp order
 // through shared memory -- and store the run's row (deterministic).
 template <typename T, int NV>
-__device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * NV], int gi,
+__device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * NV], int c,
                                            int cb, int C) {
   using V = Vec<T>;
   constexpr int NWF = SC_THREADS / 32;
   constexpr int UNR = 4;
-  constexpr int GSPAN = SC_GROUP * SC_CHUNK;
   const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
   const T* P = reinterpret_cast<const T*>(a.partial);
   T* M = reinterpret_cast<T*>(a.M);
-  const int iend = min(a.K, (gi + 1) * GSPAN);
+  const int iend = min(a.K, (c + 1) * SC_CHUNK);
   const int u = __ldcg(a.segidx + iend - 1);
-  const int g1 = (__ldcg(a.lstart + u + 1) - 1) / GSPAN;
-  const int np = g1 - gi + 1;
-  const int slot = a.zero_rows ? __ldcg(a.l2g + u) : u;
+  const int c1 = (__ldcg(a.lstart + u + 1) - 1) / SC_CHUNK;
+  const int np = c1 - c + 1;
+  const int slot = __ldcg(a.l2g + u);
   const int col0 = cb * 32 * NV + lane;
   T acc[NV];
 #pragma unroll
@@ -180,7 +169,7 @@ __device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * N
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
       const int k = k0 + q * NWF;
-      const size_t prow = k == 0 ? (size_t)(2 * gi + 1) : (size_t)(2 * (gi + k));
+      const size_t prow = k == 0 ? (size_t)(2 * c + 1) : (size_t)(2 * (c + k));
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const int col = col0 + v * 32;
@@ -209,6 +198,13 @@ __device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * N
   __syncthreads();
 }
 
+// S4 as one cooperative persistent kernel:
+//   phase 1  chunk items (segment sums -> M, partials for cut runs) and
+//            zero-row items; owners of cut runs append to the fixup list;
+//   phase 2  (after a grid barrier) the listed runs' partial sums -> M;
+//   phase 3  (world 1 only, after a grid barrier) S6: E[I^[r]] -= lr * M[r]
+//            -- with one rank the all-reduce is the identity, so the update
+//            rides in the same launch.
 __device__ __forceinline__ void sstamp(unsigned long long* tr, int i) {
   if (tr && threadIdx.x == 0) {
     unsigned long long t;
@@ -218,101 +214,44 @@ __device__ __forceinline__ void sstamp(unsigned long long* tr, int i) {
   }
 }
 
-// S4 as one persistent kernel (normal launch, co-resident grid):
-//   phase 1  group items (segment sums -> M, in-group merge of cut runs,
-//            partials at group edges) and zero-row items;
-//   phase 2  (after a grid barrier) the listed runs' partial sums -> M.
 template <typename T, int NV, int UNR>
 __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   using V = Vec<T>;
-  constexpr int NWA = SC_THREADS / 32;  // == SC_GROUP
-  constexpr int GSPAN = SC_GROUP * SC_CHUNK;
-  __shared__ T piece[NWA][2][32 * NV];  // per warp: head and tail pieces (column block)
-  __shared__ int piece_u[NWA][2];
   sstamp(a.trace, 54);
+  if (a.trace && threadIdx.x == 0) {  // earliest start over all CTAs (as ~t)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(a.trace + 63, ~t);
+  }
+  __shared__ T red[SC_THREADS / 32][32 * NV];
   const int K = a.K;
   const int C = a.D / V::W;  // vectors per row
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
   const int nchunks = (K + SC_CHUNK - 1) / SC_CHUNK;
-  const int ngroups = (nchunks + SC_GROUP - 1) / SC_GROUP;
   const int64_t Ug = a.sc3->u_global;
-  const int64_t nz = a.zero_rows ? (Ug + GSPAN - 1) / GSPAN : 0;
-  const int64_t items = ((int64_t)ngroups + nz) * ncb;
-  const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
-  const T* gr = reinterpret_cast<const T*>(a.grad);
+  const int64_t nz = a.zero_rows ? (Ug + SC_ZGROUP - 1) / SC_ZGROUP : 0;
+  const int64_t items = ((int64_t)nchunks + nz) * ncb;
+  const int lane = (int)lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* g = reinterpret_cast<const T*>(a.grad);
   T* M = reinterpret_cast<T*>(a.M);
   T* P = reinterpret_cast<T*>(a.partial);
 
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
+       it += nwarps) {
     const int cb = (int)(it % ncb);
     const int64_t unit = it / ncb;
     const int col0 = cb * 32 * NV + lane;
-    if (unit < ngroups) {
-      const int gi = (int)unit;
-      const int c = gi * SC_GROUP + warp;
-      if (lane == 0) piece_u[warp][0] = piece_u[warp][1] = -1;
-      __syncwarp();
-      if (c < nchunks) {
-        const int n = min(SC_CHUNK, K - c * SC_CHUNK);
-        if (n == SC_CHUNK && (cb + 1) * 32 * NV <= C)
-          scatter_chunk<T, NV, UNR, true>(a, gr, M, c, n, col0, C, lane, piece[warp][0],
-                                          piece[warp][1], &piece_u[warp][0], &piece_u[warp][1]);
-        else
-          scatter_chunk<T, NV, UNR, false>(a, gr, M, c, n, col0, C, lane, piece[warp][0],
-                                           piece[warp][1], &piece_u[warp][0], &piece_u[warp][1]);
-      }
-      __syncthreads();
-      if (warp == 0) {
-        // merge the group's pieces in position order
-        const int gp0 = gi * GSPAN, gp1 = min(K, gp0 + GSPAN);
-        const int left_u = gp0 > 0 ? __ldg(a.segidx + gp0 - 1) : -1;
-        const int right_u = gp1 < K ? __ldg(a.segidx + gp1) : -1;
-        T acc[NV];
-        int cur = -1;
-        auto flush = [&](int u) {
-          T* dst;
-          if (u == left_u) {
-            dst = P + (size_t)(2 * gi) * C;
-          } else if (u == right_u) {
-            dst = P + (size_t)(2 * gi + 1) * C;
-            if (cb == 0 && lane == 0) {  // this group holds the run's start: it owns the fix-up
-              const uint32_t idx = atomicAdd(&a.sc1w->fixcount, 1u);
-              if (idx < (uint32_t)a.fix_cap) a.fixlist[idx] = gi;
-            }
-          } else {
-            const int slot = a.zero_rows ? __ldg(a.l2g + u) : u;
-            dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
-          }
-          if (dst) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              const int col = col0 + v * 32;
-              if (col < C) V::st(dst + col, acc[v]);
-            }
-          }
-        };
-        for (int w = 0; w < NWA; ++w) {
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int u = piece_u[w][k];
-            if (u < 0) continue;
-            if (u != cur) {
-              if (cur >= 0) flush(cur);
-              cur = u;
-#pragma unroll
-              for (int v = 0; v < NV; ++v) acc[v] = piece[w][k][v * 32 + lane];
-            } else {
-#pragma unroll
-              for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], piece[w][k][v * 32 + lane]);
-            }
-          }
-        }
-        if (cur >= 0) flush(cur);
-      }
-      __syncthreads();
+    if (unit < nchunks) {
+      const int c = (int)unit;
+      const int n = min(SC_CHUNK, K - c * SC_CHUNK);
+      if (n == SC_CHUNK && (cb + 1) * 32 * NV <= C)
+        scatter_chunk<T, NV, UNR, true>(a, g, M, P, c, n, col0, C, lane);
+      else
+        scatter_chunk<T, NV, UNR, false>(a, g, M, P, c, n, col0, C, lane);
     } else {
-      // ---- zero rows: slots [r0, r0 + 256) whose word is absent on this rank
-      const int64_t r0 = (unit - ngroups) * GSPAN + warp * 32;
+      // ---- zero rows: slots [r0, r0 + 32) whose word is absent on this rank
+      const int64_t r0 = (unit - nchunks) * SC_ZGROUP;
       const int64_t r = r0 + lane;
       bool absent = false;
       if (r < Ug) {
@@ -336,12 +275,34 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   grid_barrier(a.bar);
   sstamp(a.trace, 56);
 
-  // phase 2: runs cut by group edges
-  T(*red)[32 * NV] = reinterpret_cast<T(*)[32 * NV]>(&piece[0][0][0]);
+  // phase 2: runs cut by chunk boundaries
   const int nfix = (int)min(__ldcg(&a.sc1w->fixcount), (uint32_t)a.fix_cap);
   for (int64_t it = blockIdx.x; it < (int64_t)nfix * ncb; it += gridDim.x)
     fixup_item<T, NV>(a, red, __ldcg(a.fixlist + it / ncb), (int)(it % ncb), C);
   sstamp(a.trace, 57);
+
+  if (!a.table) return;
+  grid_barrier(a.bar);
+
+  // phase 3 (world 1): S6 row update, warp per row
+  T* E = reinterpret_cast<T*>(a.table);
+  const float lr = a.lr;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Ug; r += nwarps) {
+    const uint32_t w = __ldg(a.ihat + r);
+    const T* src = M + (size_t)r * C;
+    T* dst = E + (size_t)w * C;
+    int col = lane;
+    for (; col + 96 < C; col += 128) {
+      const T m0 = V::ld_l2(src + col), m1 = V::ld_l2(src + col + 32);
+      const T m2 = V::ld_l2(src + col + 64), m3 = V::ld_l2(src + col + 96);
+      const T e0 = dst[col], e1 = dst[col + 32], e2 = dst[col + 64], e3 = dst[col + 96];
+      V::st(dst + col, V::fma(-lr, m0, e0));
+      V::st(dst + col + 32, V::fma(-lr, m1, e1));
+      V::st(dst + col + 64, V::fma(-lr, m2, e2));
+      V::st(dst + col + 96, V::fma(-lr, m3, e3));
+    }
+    for (; col < C; col += 32) V::st(dst + col, V::fma(-lr, V::ld_l2(src + col), dst[col]));
+  }
 }
 
 namespace {
@@ -365,12 +326,11 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   const int C = a.D / Vec<T>::W;
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
   const int64_t nchunks = (a.K + SC_CHUNK - 1) / SC_CHUNK;
-  const int64_t ngroups = (nchunks + SC_GROUP - 1) / SC_GROUP;
-  const int64_t nz = a.zero_rows ? (a.ug_cap + SC_GROUP * SC_CHUNK - 1) / (SC_GROUP * SC_CHUNK) : 0;
-  int64_t blocks = (ngroups + nz) * ncb;
+  const int64_t nz = a.zero_rows ? (a.ug_cap + SC_ZGROUP - 1) / SC_ZGROUP : 0;
+  int64_t blocks = ((nchunks + nz) * ncb * 32 + SC_THREADS - 1) / SC_THREADS;
   const int64_t cap = (int64_t)a.num_sms * occ;
   if (blocks > cap) blocks = cap;
-  if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phase 2 wants a wide grid
+  if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phases 2/3 want a wide grid
   // grid <= occupancy x SMs: every CTA is co-resident, so the in-kernel
   // grid barrier is safe with a normal launch
   k_scatter<T, NV, UNR><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
