@@ -11,6 +11,8 @@ struct GridBar;
 
 // Scatter-add chunk: sorted positions per warp work item.
 constexpr int SC_CHUNK = 32;
+// Fix-up: partial rows summed per CTA work item.
+constexpr int FX_PART = 64;
 // Zero-row group: slots per warp work item.
 constexpr int SC_ZGROUP = 32;
 
@@ -113,7 +115,8 @@ struct ScatterArgs {
   const Sc3* sc3;         // U_g
   const Sc1* sc1;         // U_i
   Sc1* sc1w;              // fixup list counter
-  int32_t* fixlist;       // owner chunks of cut runs
+  int2* fixent;           // fix-up entries: (owner chunk, part | nparts << 16)
+  float* part2;           // level-2 partial rows, one per entry (fix_cap x D)
   int fix_cap;
   int zero_rows;          // 0: every slot is present locally (world 1)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])

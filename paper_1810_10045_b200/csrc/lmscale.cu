@@ -59,7 +59,9 @@ struct lmscale_ctx {
   void* base = nullptr;
   size_t ws_bytes = 0;
   uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot;
-  int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g, *fixlist;
+  int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
+  int2* fixent;
+  float* part2;
   float* M = nullptr;
   float* partial;
   bool m_nccl = false;
@@ -290,8 +292,9 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.M = ctx->M;
   a.partial = ctx->partial;
   a.sc1w = ctx->sc1;
-  a.fixlist = ctx->fixlist;
-  a.fix_cap = (int)ctx->nchunks;
+  a.fixent = ctx->fixent;
+  a.part2 = ctx->part2;
+  a.fix_cap = (int)(2 * ctx->nchunks);
   a.zero_rows = 1;
   a.table = nullptr;
   a.lr = 0.f;
@@ -437,7 +440,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_vals_b = take(4 * K), o_segidx = take(4 * K), o_inverse = take(4 * K),
            o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)), o_counts = take(4 * K),
            o_l2g = take(4 * K), o_wrank = take(4 * ctx->W), o_I = take(4 * ctx->NI),
-           o_ihat = take(4 * ctx->ucap), o_fix = take(4 * ctx->nchunks),
+           o_ihat = take(4 * ctx->ucap), o_fix = take(8 * 2 * ctx->nchunks),
            o_bars = take(sizeof(GridBar) * 8);
     size_t o_sc3 = take(sizeof(Sc3) + sizeof(Sc1)), o_sc1 = o_sc3 + sizeof(Sc3),
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
@@ -447,6 +450,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
     const size_t m_bytes = align_up(4 * (size_t)ctx->ucap * D, 1 << 21);
     size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
+    size_t o_part2 = take(4 * (size_t)2 * ctx->nchunks * D);
     ctx->ws_bytes = off;
     if (cudaMalloc(&ctx->base, off) != cudaSuccess) {
       cudaGetLastError();
@@ -466,7 +470,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->wrank = (uint32_t*)(b + o_wrank);
     ctx->I = (uint32_t*)(b + o_I);
     ctx->ihat = (uint32_t*)(b + o_ihat);
-    ctx->fixlist = (int32_t*)(b + o_fix);
+    ctx->fixent = (int2*)(b + o_fix);
     ctx->bars = (GridBar*)(b + o_bars);
     ctx->sc1 = (Sc1*)(b + o_sc1);
     ctx->sc3 = (Sc3*)(b + o_sc3);
@@ -476,6 +480,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
     ctx->partial = (float*)(b + o_part);
+    ctx->part2 = (float*)(b + o_part2);
     CK(cudaMemset(ctx->base, 0, off));
     CK(cudaHostAlloc((void**)&ctx->h_sc3, sizeof(Sc3) + sizeof(Sc1), cudaHostAllocDefault));
     ctx->h_sc1 = (Sc1*)((char*)ctx->h_sc3 + sizeof(Sc3));

@@ -80,7 +80,8 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   const int up = __shfl_up_sync(FULL_MASK, my_u, 1);
   const unsigned hmask = __ballot_sync(FULL_MASK, (FULL || lane < n) && (lane == 0 || my_u != up));
   const bool split_left = __shfl_sync(FULL_MASK, my_u, 0) == prev_u;
-  const bool split_right = __shfl_sync(FULL_MASK, my_u, n - 1) == next_u;
+  const int u_last = __shfl_sync(FULL_MASK, my_u, n - 1);
+  const bool split_right = u_last == next_u;
   T acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = V::zero();
@@ -118,12 +119,20 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
           } else if (last && split_right) {
             dst = P + (size_t)(2 * c + 1) * C;
             // this chunk holds the start of a run cut by its end: it owns the
-            // run's fixup (listed once, by column block 0)
-            if (col0 == lane && lane == 0) {
-              const uint32_t idx = atomicAdd(&a.sc1w->fixcount, 1u);
-              if (idx < (uint32_t)a.fix_cap) a.fixlist[idx] = c;
-            }
-          } else {
+            // run's fix-up, listed (by column block 0) as ceil(np / FX_PART)
+            // contiguous parts so that long Zipf-head runs are summed by many CTAs
+            if (col0 == lane) {
+              int ent = 0, nparts = 0;
+              if (lane == 0) {
+                const int np = (__ldg(a.lstart + u_last + 1) - 1) / SC_CHUNK - c + 1;
+                nparts = (np + FX_PART - 1) / FX_PART;
+                ent = (int)atomicAdd(&a.sc1w->fixcount, (uint32_t)nparts);
+              }
+              ent = __shfl_sync(FULL_MASK, ent, 0);
+              nparts = __shfl_sync(FULL_MASK, nparts, 0);
+              for (int j = lane; j < nparts; j += 32)
+                if (ent + j < a.fix_cap) a.fixent[ent + j] = make_int2(c, j | (nparts << 16));
+            }          } else {
             dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
           }
           if (dst) {
@@ -142,29 +151,31 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   }
 }
 
-// Phase 2 (fixup) for one (owner chunk c, column block): sum the run's
-// partials P[2c+1] (tail of c) and P[2c'] (heads of c < c' <= c1) in a fixed
-// order -- warp w sums partials w, w+8, ...; warps are combined in warp order
-// through shared memory -- and store the run's row (deterministic).
+// Phase 2a (fix-up part) for one listed entry (owner chunk c, part j of
+// nparts) and column block: sum partials k in [64j, min(np, 64j + 64)) of the
+// run -- k = 0 is P[2c+1] (tail of c), k >= 1 is P[2(c+k)] (head of c+k) --
+// in a fixed order (warp w sums k = w, w+8, ...; warps combined in warp order
+// through shared memory).  One part: the sum is the run's row of M.  More
+// parts: it goes to level-2 row `e` and phase 2b adds the parts in order.
 template <typename T, int NV>
-__device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * NV], int c,
+__device__ __forceinline__ void fixup_part(const ScatterArgs& a, T (*red)[32 * NV], int e,
                                            int cb, int C) {
   using V = Vec<T>;
   constexpr int NWF = SC_THREADS / 32;
   constexpr int UNR = 4;
   const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
   const T* P = reinterpret_cast<const T*>(a.partial);
-  T* M = reinterpret_cast<T*>(a.M);
+  const int2 en = __ldcg(a.fixent + e);
+  const int c = en.x, j = en.y & 0xffff, nparts = en.y >> 16;
   const int iend = min(a.K, (c + 1) * SC_CHUNK);
   const int u = __ldcg(a.segidx + iend - 1);
-  const int c1 = (__ldcg(a.lstart + u + 1) - 1) / SC_CHUNK;
-  const int np = c1 - c + 1;
-  const int slot = __ldcg(a.l2g + u);
+  const int np = (__ldcg(a.lstart + u + 1) - 1) / SC_CHUNK - c + 1;
+  const int k_lo = j * FX_PART, k_hi = min(np, k_lo + FX_PART);
   const int col0 = cb * 32 * NV + lane;
   T acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-  for (int k0 = warp; k0 < np; k0 += NWF * UNR) {
+  for (int k0 = k_lo + warp; k0 < k_hi; k0 += NWF * UNR) {
     T r[UNR][NV];
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
@@ -174,7 +185,7 @@ __device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * N
       for (int v = 0; v < NV; ++v) {
         const int col = col0 + v * 32;
         r[q][v] = V::zero();
-        if (k < np && col < C) r[q][v] = V::ld_l2(P + prow * C + col);
+        if (k < k_hi && col < C) r[q][v] = V::ld_l2(P + prow * C + col);
       }
     }
 #pragma unroll
@@ -185,26 +196,52 @@ __device__ __forceinline__ void fixup_item(const ScatterArgs& a, T (*red)[32 * N
 #pragma unroll
   for (int v = 0; v < NV; ++v) red[warp][v * 32 + lane] = acc[v];
   __syncthreads();
-  if (warp == 0 && slot >= 0) {
+  if (warp == 0) {
+    T* dst;
+    if (nparts == 1) {
+      const int slot = a.zero_rows ? __ldcg(a.l2g + u) : u;
+      dst = slot >= 0 ? reinterpret_cast<T*>(a.M) + (size_t)slot * C : nullptr;
+    } else {
+      dst = reinterpret_cast<T*>(a.part2) + (size_t)e * C;
+    }
+    if (dst) {
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      T sum = red[0][v * 32 + lane];
+      for (int v = 0; v < NV; ++v) {
+        T sum = red[0][v * 32 + lane];
 #pragma unroll
-      for (int w = 1; w < NWF; ++w) sum = V::add(sum, red[w][v * 32 + lane]);
-      const int col = col0 + v * 32;
-      if (col < C) V::st(M + (size_t)slot * C + col, sum);
+        for (int w = 1; w < NWF; ++w) sum = V::add(sum, red[w][v * 32 + lane]);
+        const int col = col0 + v * 32;
+        if (col < C) V::st(dst + col, sum);
+      }
     }
   }
   __syncthreads();
 }
 
-// S4 as one cooperative persistent kernel:
-//   phase 1  chunk items (segment sums -> M, partials for cut runs) and
-//            zero-row items; owners of cut runs append to the fixup list;
-//   phase 2  (after a grid barrier) the listed runs' partial sums -> M;
-//   phase 3  (world 1 only, after a grid barrier) S6: E[I^[r]] -= lr * M[r]
-//            -- with one rank the all-reduce is the identity, so the update
-//            rides in the same launch.
+// Phase 2b: a run listed as nparts > 1 parts (entries e0 .. e0+nparts-1,
+// contiguous): add its level-2 rows in entry order, store the run's M row.
+template <typename T, int NV>
+__device__ __forceinline__ void fixup_final(const ScatterArgs& a, int e0, int cb, int C) {
+  using V = Vec<T>;
+  const int lane = (int)lane_id();
+  const int2 en = __ldcg(a.fixent + e0);
+  const int c = en.x, nparts = en.y >> 16;
+  const int iend = min(a.K, (c + 1) * SC_CHUNK);
+  const int u = __ldcg(a.segidx + iend - 1);
+  const int slot = a.zero_rows ? __ldcg(a.l2g + u) : u;
+  if (slot < 0) return;
+  const T* L2 = reinterpret_cast<const T*>(a.part2);
+  const int col0 = cb * 32 * NV + lane;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int col = col0 + v * 32;
+    if (col >= C) continue;
+    T sum = V::ld_l2(L2 + (size_t)e0 * C + col);
+    for (int j = 1; j < nparts; ++j) sum = V::add(sum, V::ld_l2(L2 + (size_t)(e0 + j) * C + col));
+    V::st(reinterpret_cast<T*>(a.M) + (size_t)slot * C + col, sum);
+  }
+}
+
 __device__ __forceinline__ void sstamp(unsigned long long* tr, int i) {
   if (tr && threadIdx.x == 0) {
     unsigned long long t;
@@ -275,11 +312,20 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   grid_barrier(a.bar);
   sstamp(a.trace, 56);
 
-  // phase 2: runs cut by chunk boundaries
+  // phase 2a: parts of the runs cut by chunk boundaries (balanced: <= FX_PART
+  // partials per CTA item)
   const int nfix = (int)min(__ldcg(&a.sc1w->fixcount), (uint32_t)a.fix_cap);
   for (int64_t it = blockIdx.x; it < (int64_t)nfix * ncb; it += gridDim.x)
-    fixup_item<T, NV>(a, red, __ldcg(a.fixlist + it / ncb), (int)(it % ncb), C);
+    fixup_part<T, NV>(a, red, (int)(it / ncb), (int)(it % ncb), C);
   sstamp(a.trace, 57);
+  grid_barrier(a.bar);
+  // phase 2b: runs split into several parts, one warp per (run, column block)
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t it = gwarp; it < (int64_t)nfix * ncb; it += nwarps) {
+    const int e = (int)(it / ncb);
+    const int2 en = __ldcg(a.fixent + e);
+    if ((en.y & 0xffff) == 0 && (en.y >> 16) > 1) fixup_final<T, NV>(a, e, (int)(it % ncb), C);
+  }
 
   if (!a.table) return;
   grid_barrier(a.bar);
