@@ -13,6 +13,9 @@ struct GridBar;
 constexpr int SC_CHUNK = 32;
 // Fix-up: partial rows summed per CTA work item.
 constexpr int FX_PART = 64;
+// Runs of <= FX_SHORT tokens are summed whole by the chunk holding their start
+// (<= SC_CHUNK: the read-on past a chunk edge stays within one more chunk).
+constexpr int FX_SHORT = 32;
 // Zero-row group: slots per warp work item.
 constexpr int SC_ZGROUP = 32;
 

@@ -59,72 +59,93 @@ constexpr unsigned FULL_MASK = 0xffffffffu;
 
 // ------------------------------------------------------------------- S4
 
-// One chunk of sorted positions [i0, i0 + n) for one column block.  FULL:
-// n == SC_CHUNK and the column block lies inside the row (no predicates).
-template <typename T, int NV, int UNR, bool FULL>
+// One chunk of sorted positions [i0, i0 + n) for one column block.  Runs of
+// <= FX_SHORT tokens belong entirely to the chunk where they start: a short
+// run cut by the chunk's right edge is finished by reading on (at most
+// FX_SHORT - 1 positions past the edge) and the next chunk skips its tail.
+// Only long runs (the Zipf head) are cut into partial rows (P[2c] head piece,
+// P[2c+1] tail piece) and listed for the fix-up phase by the chunk holding
+// their start.  FULLC: the column block lies inside the row (no predicates).
+template <typename T, int NV, int UNR, bool FULLC>
 __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __restrict__ g,
                                               T* __restrict__ M, T* __restrict__ P, int c,
                                               int n, int col0, int C, int lane) {
   using V = Vec<T>;
   const int K = a.K;
   const int i0 = c * SC_CHUNK;
-  int my_pos = 0, my_u = -1, my_slot = -1;
-  if (FULL || lane < n) {
+  int my_pos = 0, my_u = -1;
+  if (lane < n) {
     my_pos = __ldg(a.perm + i0 + lane);
     my_u = __ldg(a.segidx + i0 + lane);
   }
   const int prev_u = i0 > 0 ? __ldg(a.segidx + i0 - 1) : -1;
   const int next_u = i0 + n < K ? __ldg(a.segidx + i0 + n) : -1;
-  // world 1: I^ = J^, so the slot is the run index itself (no dependent load)
-  if (FULL || lane < n) my_slot = a.zero_rows ? __ldg(a.l2g + my_u) : my_u;
   const int up = __shfl_up_sync(FULL_MASK, my_u, 1);
-  const unsigned hmask = __ballot_sync(FULL_MASK, (FULL || lane < n) && (lane == 0 || my_u != up));
-  const bool split_left = __shfl_sync(FULL_MASK, my_u, 0) == prev_u;
+  const unsigned hmask = __ballot_sync(FULL_MASK, lane < n && (lane == 0 || my_u != up));
+  const int u_first = __shfl_sync(FULL_MASK, my_u, 0);
   const int u_last = __shfl_sync(FULL_MASK, my_u, n - 1);
+  const bool split_left = u_first == prev_u;
   const bool split_right = u_last == next_u;
+  // run extents of the cut runs: lanes 0..3 load lstart[u_first], lstart[u_first+1],
+  // lstart[u_last], lstart[u_last+1]
+  int ls = 0;
+  if ((lane < 2 && split_left) || (lane >= 2 && lane < 4 && split_right))
+    ls = __ldg(a.lstart + (lane < 2 ? u_first + lane : u_last + lane - 2));
+  // world 1: I^ = J^, so the slot is the run index itself (no dependent load)
+  int my_slot = -1;
+  if (lane < n) my_slot = a.zero_rows ? __ldg(a.l2g + my_u) : my_u;
+  const int f_start = __shfl_sync(FULL_MASK, ls, 0), f_end = __shfl_sync(FULL_MASK, ls, 1);
+  const int l_start = __shfl_sync(FULL_MASK, ls, 2), l_end = __shfl_sync(FULL_MASK, ls, 3);
+  const bool first_long = split_left && (f_end - f_start > FX_SHORT);
+  const bool last_long = split_right && (l_end - l_start > FX_SHORT);
+  // [p_begin, p_end): positions this chunk sums (p_end may pass n for a short
+  // run started here and cut by the right edge)
+  const int p_begin = (split_left && !first_long) ? min(n, f_end - i0) : 0;
+  if (p_begin >= n) return;  // the whole chunk is the tail of a short run owned earlier
+  const bool extend = split_right && !last_long;
+  const int p_end = extend ? l_end - i0 : n;
+  int ext_pos = 0;
+  if (extend && SC_CHUNK + lane < p_end) ext_pos = __ldg(a.perm + i0 + SC_CHUNK + lane);
   T acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-  bool seg_first = true;  // the run being accumulated is the chunk's first
-  for (int p0 = 0; p0 < n; p0 += UNR) {
+  bool seg_first = (p_begin == 0);  // the run being accumulated is the chunk's first
+  for (int p0 = p_begin; p0 < p_end; p0 += UNR) {
     T r[UNR][NV];
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
       const int p = p0 + q;
-      const int pos = __shfl_sync(FULL_MASK, my_pos, p & 31);
+      const int pos = p < SC_CHUNK ? __shfl_sync(FULL_MASK, my_pos, p & 31)
+                                   : __shfl_sync(FULL_MASK, ext_pos, p & 31);
       const T* row = g + (size_t)pos * C;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const int col = col0 + v * 32;
-        if (FULL) {
-          r[q][v] = V::ld_once(row + col);
-        } else {
-          r[q][v] = V::zero();
-          if (p < n && col < C) r[q][v] = V::ld_once(row + col);
-        }
+        r[q][v] = V::zero();
+        if (p < p_end && (FULLC || col < C)) r[q][v] = V::ld_once(row + col);
       }
     }
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
       const int p = p0 + q;
-      if (FULL || p < n) {
+      if (p < p_end) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
-        const bool last = (p == n - 1);
-        if (last || ((hmask >> (p + 1)) & 1u)) {
-          const int slot = __shfl_sync(FULL_MASK, my_slot, p);
+        const bool last = (p == p_end - 1);
+        if (last || (p + 1 < n && ((hmask >> (p + 1)) & 1u))) {
+          const int slot = __shfl_sync(FULL_MASK, my_slot, min(p, n - 1));
           T* dst;
-          if (seg_first && split_left) {
+          if (seg_first && split_left) {  // long run continuing from the left
             dst = P + (size_t)(2 * c) * C;
-          } else if (last && split_right) {
+          } else if (last && split_right && last_long) {
             dst = P + (size_t)(2 * c + 1) * C;
-            // this chunk holds the start of a run cut by its end: it owns the
-            // run's fix-up, listed (by column block 0) as ceil(np / FX_PART)
-            // contiguous parts so that long Zipf-head runs are summed by many CTAs
+            // this chunk holds the start of a long run cut by its end: it owns
+            // the run's fix-up, listed (by column block 0) as ceil(np / FX_PART)
+            // contiguous parts so that the Zipf head is summed by many CTAs
             if (col0 == lane) {
               int ent = 0, nparts = 0;
               if (lane == 0) {
-                const int np = (__ldg(a.lstart + u_last + 1) - 1) / SC_CHUNK - c + 1;
+                const int np = (l_end - 1) / SC_CHUNK - c + 1;
                 nparts = (np + FX_PART - 1) / FX_PART;
                 ent = (int)atomicAdd(&a.sc1w->fixcount, (uint32_t)nparts);
               }
@@ -132,14 +153,15 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
               nparts = __shfl_sync(FULL_MASK, nparts, 0);
               for (int j = lane; j < nparts; j += 32)
                 if (ent + j < a.fix_cap) a.fixent[ent + j] = make_int2(c, j | (nparts << 16));
-            }          } else {
+            }
+          } else {
             dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
           }
           if (dst) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
               const int col = col0 + v * 32;
-              if (FULL || col < C) V::st(dst + col, acc[v]);
+              if (FULLC || col < C) V::st(dst + col, acc[v]);
             }
           }
 #pragma unroll
@@ -282,7 +304,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
     if (unit < nchunks) {
       const int c = (int)unit;
       const int n = min(SC_CHUNK, K - c * SC_CHUNK);
-      if (n == SC_CHUNK && (cb + 1) * 32 * NV <= C)
+      if ((cb + 1) * 32 * NV <= C)
         scatter_chunk<T, NV, UNR, true>(a, g, M, P, c, n, col0, C, lane);
       else
         scatter_chunk<T, NV, UNR, false>(a, g, M, P, c, n, col0, C, lane);
