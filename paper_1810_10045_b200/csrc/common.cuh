@@ -115,22 +115,26 @@ struct GridBar {
   uint32_t count;
   uint32_t gen;
 };
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
 __device__ __forceinline__ void grid_barrier(GridBar* b) {
-  __syncthreads();
+  __syncthreads();  // the CTA's writes happen-before thread 0's release below
   if (threadIdx.x == 0) {
     const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
     const uint32_t gen = ld_acquire(&b->gen);
-    __threadfence();
-    if (atomicAdd(&b->count, 1u) == nb - 1) {
-      b->count = 0u;
-      __threadfence();
+    if (atom_add_acq_rel(&b->count, 1u) == nb - 1) {
+      b->count = 0u;                 // ordered before the release of gen
       st_release(&b->gen, gen + 1u);
     } else {
-      while (ld_acquire(&b->gen) == gen) __nanosleep(32);
+      while (ld_acquire(&b->gen) == gen) {
+      }
     }
-    __threadfence();
   }
-  __syncthreads();
+  __syncthreads();  // thread 0's acquire happens-before the CTA's reads
 }
 
 // One carveout for every kernel of the library (max shared memory): the SMs

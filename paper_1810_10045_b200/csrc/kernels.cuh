@@ -122,6 +122,7 @@ struct ScatterArgs {
   float* part2;           // level-2 partial rows, one per entry (fix_cap x D)
   int fix_cap;
   int zero_rows;          // 0: every slot is present locally (world 1)
+  int short_runs;         // finish runs <= FX_SHORT in their starting chunk (large K)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
   float lr;
   unsigned long long* trace;

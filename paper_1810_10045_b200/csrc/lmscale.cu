@@ -296,6 +296,7 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.part2 = ctx->part2;
   a.fix_cap = (int)(2 * ctx->nchunks);
   a.zero_rows = 1;
+  a.short_runs = ctx->last_k >= (1 << 16) ? 1 : 0;
   a.table = nullptr;
   a.lr = 0.f;
   a.trace = ctx->trace;

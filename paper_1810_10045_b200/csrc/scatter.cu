@@ -96,8 +96,10 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   if (lane < n) my_slot = a.zero_rows ? __ldg(a.l2g + my_u) : my_u;
   const int f_start = __shfl_sync(FULL_MASK, ls, 0), f_end = __shfl_sync(FULL_MASK, ls, 1);
   const int l_start = __shfl_sync(FULL_MASK, ls, 2), l_end = __shfl_sync(FULL_MASK, ls, 3);
-  const bool first_long = split_left && (f_end - f_start > FX_SHORT);
-  const bool last_long = split_right && (l_end - l_start > FX_SHORT);
+  // without short-run handling (small K, where the fix-up is cheap) every cut
+  // run is treated as long: no run-extent lookup before the row loop
+  const bool first_long = split_left && (!a.short_runs || f_end - f_start > FX_SHORT);
+  const bool last_long = split_right && (!a.short_runs || l_end - l_start > FX_SHORT);
   // [p_begin, p_end): positions this chunk sums (p_end may pass n for a short
   // run started here and cut by the right edge)
   const int p_begin = (split_left && !first_long) ? min(n, f_end - i0) : 0;
