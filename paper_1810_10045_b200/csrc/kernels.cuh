@@ -12,7 +12,7 @@ struct GridBar;
 // Scatter-add chunk: sorted positions per warp work item.
 constexpr int SC_CHUNK = 32;
 // Fix-up: partial rows summed per CTA work item.
-constexpr int FX_PART = 64;
+constexpr int FX_PART = 128;
 // Runs of <= FX_SHORT tokens are summed whole by the chunk holding their start
 // (<= SC_CHUNK: the read-on past a chunk edge stays within one more chunk).
 constexpr int FX_SHORT = 32;
@@ -22,7 +22,7 @@ constexpr int SC_ZGROUP = 32;
 // Per-step device scalars of S1 (zeroed at the start of S1).
 struct Sc1 {
   int64_t u_local;
-  uint32_t err;        // bit 0: an id >= vocab seen by S1
+  uint32_t err;        // bit 0: an id >= vocab seen by S1; bit 1: S4 split a run into fix-up parts
   uint32_t fixcount;   // S4: runs cut by chunk boundaries (zeroed by S1)
 };
 // Per-step device scalars of S3 (zeroed at the start of S3).

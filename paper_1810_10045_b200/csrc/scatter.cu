@@ -150,6 +150,7 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
                 const int np = (l_end - 1) / SC_CHUNK - c + 1;
                 nparts = (np + FX_PART - 1) / FX_PART;
                 ent = (int)atomicAdd(&a.sc1w->fixcount, (uint32_t)nparts);
+                if (nparts > 1) atomicOr(&a.sc1w->err, 2u);  // phase 2b needed
               }
               ent = __shfl_sync(FULL_MASK, ent, 0);
               nparts = __shfl_sync(FULL_MASK, nparts, 0);
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   for (int64_t it = blockIdx.x; it < (int64_t)nfix * ncb; it += gridDim.x)
     fixup_part<T, NV>(a, red, (int)(it / ncb), (int)(it % ncb), C);
   sstamp(a.trace, 57);
+  if (!(__ldcg(&a.sc1w->err) & 2u)) return;  // no run was split into parts
   grid_barrier(a.bar);
   // phase 2b: runs split into several parts, one warp per (run, column block)
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
