@@ -171,13 +171,22 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
         for (int k = 0; k < dpt; ++k) {
           const uint32_t* row = cT + (size_t)(d0 + k) * a.ntp;
           uint32_t pr = 0, to = 0;
-          for (int t4 = 0; t4 < a.ntp; t4 += 4) {
-            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + t4));
-            const uint32_t c4[4] = {v.x, v.y, v.z, v.w};
+          // 8 independent 128-bit loads in flight per batch (rows are L2-resident)
+          for (int t0 = 0; t0 < a.ntp; t0 += 32) {
+            uint4 v[8];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              to += c4[e];
-              pr += (t4 + e < t) ? c4[e] : 0u;
+            for (int q = 0; q < 8; ++q)
+              v[q] = (t0 + 4 * q < a.ntp) ? __ldcg(reinterpret_cast<const uint4*>(row + t0 + 4 * q))
+                                          : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t c4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int tt = t0 + 4 * q + e;
+                to += c4[e];
+                pr += (tt < t) ? c4[e] : 0u;
+              }
             }
           }
           pre[k] = pr;
