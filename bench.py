@@ -173,7 +173,9 @@ def run_reference(args, cfg, rank, world):
 def config_dict(cfg, args, world):
     return {"workload": cfg.name, "V": cfg.V, "K_per_gpu": cfg.K, "D": cfg.D, "zipf_s": cfg.s,
             "G": world, "value_mode": args.mode, "global_tokens": world * cfg.K,
-            "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read sweep), "
+                  "outside the timed region",
             "cuda_graph": not getattr(args, "no_graph", True)}
 
 
@@ -220,6 +222,16 @@ def main():
     grad = synth.grad_values(cfg.K, cfg.D, args.mode, rank=rank, device=dev)
     lr = synth.default_lr(args.mode)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    sweep = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    sweep.zero_()
+    sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def flush_l2():
+        # write a buffer larger than L2, then read another one: L2 ends up
+        # holding clean, unrelated lines (the flush's own write-backs are not
+        # charged to the timed step)
+        flush.zero_()
+        torch.sum(sweep, out=sink)
 
     flags = 0 if args.no_graph else lmscale.FLAG_GRAPH
     if world > 1:
@@ -250,7 +262,7 @@ def main():
         for i in range(steps):
             if world > 1:
                 dist.barrier()     # ranks enter each timed step together (outside the events)
-            flush.zero_()
+            flush_l2()
             ev[i][0].record(stream)
             fn()
             ev[i][1].record(stream)
