@@ -231,7 +231,7 @@ def main():
         # holding clean, unrelated lines (the flush's own write-backs are not
         # charged to the timed step)
         flush.zero_()
-        torch.sum(sweep, out=sink)
+        torch.sum(sweep, dim=(0,), out=sink.view(()))
 
     flags = 0 if args.no_graph else lmscale.FLAG_GRAPH
     if world > 1:
