@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches (no CUDA graph)")
+    ap.add_argument("--s4-events", type=int, default=1,
+                    help="1: bracket S4 with events inside the timed steps (roofline); 0: none")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
@@ -291,11 +293,13 @@ def main():
                  if "CUDA_VISIBLE_DEVICES" in os.environ else local)
     # Timed region: only the two events that bracket the S4 kernel are
     # recorded inside the step (each event node costs ~3 us of GPU time).
-    ctx.set_timing(1)
+    ctx.set_timing(args.s4_events)
     scat = []
 
     def collect_s4():
-        scat.append(ctx.stats()["us_scatter"])
+        v = ctx.stats()["us_scatter"]
+        if v > 0:
+            scat.append(v)
     clk.start()
     for _ in range(args.warmup):
         step()
@@ -318,7 +322,7 @@ def main():
     # per-phase device times (median over timed steps), max over ranks
     ph = {k: max_over_ranks(statistics.median(v), dev) for k, v in phase.items() if v}
     ph["note"] = "diagnostic pass with an event around every phase (~3 us each); not the timed region"
-    s4_us = max_over_ranks(statistics.median(scat), dev)
+    s4_us = max_over_ranks(statistics.median(scat) if scat else ph["us_scatter"], dev)
     hbm_peak, peak_kind = peaks()
     st_last = ctx.stats()
     D = cfg.D
