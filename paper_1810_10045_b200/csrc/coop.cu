@@ -157,50 +157,72 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
     stamp(a.trace, 1 + 4 * p);
     grid_barrier(a.bar);
     stamp(a.trace, 2 + 4 * p);
-    // P2: bases from the digit-major count rows, then the stable scatter
+    // Bases, distributed: CTA b owns digits [r0, r1).  A warp per digit scans
+    // the digit's per-tile counts (one coalesced row of cT) into per-tile
+    // exclusive prefixes; the CTA scans its digits' totals; range offsets are
+    // combined across CTAs; every tile's bases land tile-major in bT.
+    {
+      const int nb = (int)gridDim.x;
+      const int r0 = (int)((int64_t)ndig * blockIdx.x / nb);
+      const int r1 = (int)((int64_t)ndig * (blockIdx.x + 1) / nb);
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int d = r0 + warp; d < r1; d += NW) {
+        const uint32_t* row = cT + (size_t)d * a.ntp;
+        uint32_t carry = 0;
+        for (int t0 = 0; t0 < a.ntiles; t0 += 32) {
+          const int t = t0 + lane;
+          const uint32_t v = t < a.ntiles ? __ldcg(row + t) : 0u;
+          uint32_t x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+          }
+          if (t < a.ntiles) a.bT[(size_t)t * ndig + d] = carry + x - v;  // exclusive over tiles
+          carry += __shfl_sync(FULL, x, 31);
+        }
+        if (lane == 0) s_base[d - r0] = carry;  // digit total
+      }
+      __syncthreads();
+      // exclusive scan of this range's digit totals (<= 2048 / nb digits)
+      const int nr = r1 - r0;
+      const int dpt2 = (nr + CT - 1) / CT;
+      uint32_t dt[8], my = 0;
+      for (int k = 0; k < dpt2 && k < 8; ++k) {
+        const int dl = tid * dpt2 + k;
+        dt[k] = dl < nr ? s_base[dl] : 0u;
+        my += dt[k];
+      }
+      uint32_t rtot;
+      uint32_t ex = block_excl_scan(my, s_scan, &rtot);
+      __syncthreads();
+      for (int k = 0; k < dpt2 && k < 8; ++k) {
+        const int dl = tid * dpt2 + k;
+        if (dl < nr) s_base[dl] = ex;
+        ex += dt[k];
+      }
+      if (tid == 0) a.rtot[blockIdx.x] = rtot;
+      stamp(a.trace, 9 + 3 * p);
+      grid_barrier(a.bar);
+      uint32_t part = 0;
+      for (int c = tid; c < (int)blockIdx.x; c += CT) part += __ldcg(a.rtot + c);
+      const uint32_t roff = block_sum(part, s_scan);
+      for (int i = tid; i < nr * a.ntiles; i += CT) {
+        const int t = i / nr, dl = i % nr;
+        uint32_t* pb = a.bT + (size_t)t * ndig + r0 + dl;
+        *pb = __ldcg(pb) + roff + s_base[dl];
+      }
+      stamp(a.trace, 10 + 3 * p);
+      grid_barrier(a.bar);
+      stamp(a.trace, 11 + 3 * p);
+    }
+    // P2: this tile's bases (one coalesced row), then the stable scatter
     for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
       if (!single) {
         rank_tile(kin, vin, K, t, shift, ndig, s_cnt, key, val, rank, dig);
         warp_offsets(s_cnt, ndig, nullptr, a.ntp, t);
       }
-      // each thread owns digits [d0, d0 + dpt)
-      const int dpt = ndig > CT ? ndig / CT : 1;
-      const int d0 = tid * dpt;
-      uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
-      if (d0 < ndig) {
-        for (int k = 0; k < dpt; ++k) {
-          const uint32_t* row = cT + (size_t)(d0 + k) * a.ntp;
-          uint32_t pr = 0, to = 0;
-          // 8 independent 128-bit loads in flight per batch (rows are L2-resident)
-          for (int t0 = 0; t0 < a.ntp; t0 += 32) {
-            uint4 v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              v[q] = (t0 + 4 * q < a.ntp) ? __ldcg(reinterpret_cast<const uint4*>(row + t0 + 4 * q))
-                                          : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const uint32_t c4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int tt = t0 + 4 * q + e;
-                to += c4[e];
-                pr += (tt < t) ? c4[e] : 0u;
-              }
-            }
-          }
-          pre[k] = pr;
-          tot[k] = to;
-        }
-      }
-      uint32_t mysum = tot[0] + tot[1] + tot[2] + tot[3], all;
-      uint32_t ex = block_excl_scan(mysum, s_scan, &all);
-      if (d0 < ndig) {
-        for (int k = 0; k < dpt; ++k) {
-          s_base[d0 + k] = ex + pre[k];
-          ex += tot[k];
-        }
-      }
+      for (int d = tid; d < ndig; d += CT) s_base[d] = __ldcg(a.bT + (size_t)t * ndig + d);
       __syncthreads();
       const int warp = tid >> 5;
 #pragma unroll

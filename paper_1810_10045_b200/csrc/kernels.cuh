@@ -52,6 +52,8 @@ struct S1Args {
   uint32_t *ka, *kb;
   int32_t *va, *vb;
   uint32_t* cT;  // [passes][1 << bits][ntp] digit-major per-tile counts
+  uint32_t* bT;  // [ntiles][1 << bits] tile-major bases (one pass at a time)
+  uint32_t* rtot;  // [grid] digit-range totals
   int ntiles, ntp;
   uint32_t* luniq;
   int32_t* lstart;

@@ -58,7 +58,7 @@ struct lmscale_ctx {
   // device workspace
   void* base = nullptr;
   size_t ws_bytes = 0;
-  uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot;
+  uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot, *bT;
   int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
   int2* fixent;
   float* part2;
@@ -195,6 +195,8 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   a.va = ctx->vals_a;
   a.vb = ctx->vals_b;
   a.cT = ctx->cT;
+  a.bT = ctx->bT;
+  a.rtot = ctx->ctot;
   a.ntiles = (int)((k + CO_TILE - 1) / CO_TILE);
   a.ntp = (a.ntiles + 3) / 4 * 4;
   a.luniq = ctx->luniq;
@@ -446,6 +448,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     size_t o_sc3 = take(sizeof(Sc3) + sizeof(Sc1)), o_sc1 = o_sc3 + sizeof(Sc3),
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
            o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
+           o_bT = take(4 * (size_t)ctx->ntiles_max * (1u << ctx->plan.bits)),
            o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W);
     // M lives in its own allocation: with a communicator it comes from
     // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
@@ -477,6 +480,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->sc3 = (Sc3*)(b + o_sc3);
     ctx->cT = (uint32_t*)(b + o_cT);
     ctx->heads = (uint32_t*)(b + o_heads);
+    ctx->bT = (uint32_t*)(b + o_bT);
     ctx->ctot = (uint32_t*)(b + o_ctot);
     ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
