@@ -268,6 +268,8 @@ def main():
             ev[i][1].record(stream)
             if collect:
                 collect()
+            else:
+                torch.cuda.synchronize()   # keep ranks in lock-step (outside the events)
         barrier()
         ms = [a.elapsed_time(b) for a, b in ev]
         return ms
