@@ -72,8 +72,8 @@ class Clocks:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, device_index):
-        self.idx = device_index
+    def __init__(self, device_indices):
+        self.idx = ",".join(str(i) for i in device_indices)
         self.proc = None
         self.lines = []
 
@@ -289,18 +289,35 @@ def main():
             phase[k].append(st[k])
         info["u_local"] = st["u_local"]
 
-    clk = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
-                 if "CUDA_VISIBLE_DEVICES" in os.environ else local)
+    # One nvidia-smi sampler, on rank 0, for every rank's GPU (one sampler per
+    # rank was measured to perturb multi-GPU steps).  It runs through a
+    # ~0.3 s untimed load window, the timed region and a short tail, so the
+    # samples cover the timed region even when it lasts under a millisecond.
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    phys = [int(x) for x in vis.split(",")][:world] if vis else list(range(world))
+    clk = Clocks(phys) if rank == 0 else None
+
+    def load_window(seconds):
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end:
+            for _ in range(8):
+                step()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     # Timed region (value): no events inside the step (each event node is a
     # GPU-side serialisation point worth several microseconds).
     ctx.set_timing(0)
-    clk.start()
     for _ in range(args.warmup):
         step()
+    if clk:
+        clk.start()
+    load_window(0.3)
     k_before = ctx.stats()["kernels_total_lo"]
     ms = timed(step, args.steps, 0)
     launches[0] = ctx.stats()["kernels_total_lo"] - k_before
-    clocks = clk.stop()
+    load_window(0.1)
+    clocks = clk.stop() if clk else None
     info["ug"] = ctx.sparse_grad().num_unique
     # Second timed pass, same steps, with the two events that bracket the S4
     # kernel: its live per-launch duration for the roofline.
