@@ -427,6 +427,7 @@ def main():
                 "phases_us_diagnostic": ph, "roofline": roof, "roofline_s5_s6": upd,
                 "dense_baseline": dense, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": sync_launches, "gpu_launches_per_step": sync_launches / args.steps,
+                "step_us_rank0": [round(1e3 * x, 1) for x in ms],
                 "library": lmscale.version()}
         emit(line, args)
     ctx.close()
