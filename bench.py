@@ -298,13 +298,24 @@ def main():
     clk = Clocks(phys) if rank == 0 else None
 
     def load_window(seconds):
-        t_end = time.perf_counter() + seconds
-        while time.perf_counter() < t_end:
+        # a fixed number of steps, the same on every rank (collectives must
+        # match): sized from rank 0's timing of one batch of 8 steps
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(8):
+            step()
+        torch.cuda.synchronize()
+        per = max(time.perf_counter() - t0, 1e-6) / 8
+        n = torch.tensor([int(seconds / per) // 8 + 1], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.broadcast(n, 0)
+        for _ in range(int(n.item())):
             for _ in range(8):
                 step()
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+
     # Timed region (value): no events inside the step (each event node is a
     # GPU-side serialisation point worth several microseconds).
     ctx.set_timing(0)
