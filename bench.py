@@ -79,10 +79,12 @@ class Clocks:
 
     def start(self):
         try:
+            interval = os.environ.get("BENCH_CLOCK_MS", "200")
+            nice = ["nice", "-n", "19"] if os.environ.get("BENCH_CLOCK_NICE") else []
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx),
+                nice + ["nvidia-smi", "-i", str(self.idx),
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", interval],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -295,7 +297,7 @@ def main():
     # samples cover the timed region even when it lasts under a millisecond.
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     phys = [int(x) for x in vis.split(",")][:world] if vis else list(range(world))
-    clk = Clocks(phys) if rank == 0 else None
+    clk = Clocks(phys) if rank == 0 and not os.environ.get("BENCH_NO_CLOCKS") else None
 
     def load_window(seconds):
         # a fixed number of steps, the same on every rank (collectives must
