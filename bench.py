@@ -261,17 +261,16 @@ def main():
         barrier()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(steps)]
+        # steps are enqueued back to back (no host round trip between them);
+        # each is bracketed by its own events, the L2 flush between steps is
+        # outside them, and the step's own collectives keep ranks in lock-step
         for i in range(steps):
-            if world > 1:
-                dist.barrier()     # ranks enter each timed step together (outside the events)
             flush_l2()
             ev[i][0].record(stream)
             fn()
             ev[i][1].record(stream)
             if collect:
                 collect()
-            else:
-                torch.cuda.synchronize()   # keep ranks in lock-step (outside the events)
         barrier()
         ms = [a.elapsed_time(b) for a, b in ev]
         return ms
