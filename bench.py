@@ -345,6 +345,10 @@ def main():
     ctx.set_timing(2)
     timed(step, 3, 1, collect)
     ctx.set_timing(0)
+    all_ms = [ms]
+    if world > 1:
+        all_ms = [None] * world
+        dist.all_gather_object(all_ms, [round(1e3 * x, 1) for x in ms])
     total_ms = max_over_ranks(sum(ms), dev)
     ms_step = total_ms / args.steps
     tokens = world * cfg.K
@@ -439,7 +443,7 @@ def main():
                 "phases_us_diagnostic": ph, "roofline": roof, "roofline_s5_s6": upd,
                 "dense_baseline": dense, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": sync_launches, "gpu_launches_per_step": sync_launches / args.steps,
-                "step_us_rank0": [round(1e3 * x, 1) for x in ms],
+                "step_us_per_rank": all_ms if world > 1 else [[round(1e3 * x, 1) for x in ms]],
                 "library": lmscale.version()}
         emit(line, args)
     ctx.close()
