@@ -227,6 +227,7 @@ def main():
     sweep = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     sweep.zero_()
     sink = torch.empty(1, dtype=torch.float32, device=dev)
+    torch.sum(sweep, dim=(0,), out=sink.view(()))   # load the reduction kernel before timing
 
     def flush_l2():
         # write a buffer larger than L2, then read another one: L2 ends up
@@ -257,6 +258,7 @@ def main():
 
     def timed(fn, steps, warmup, collect=None):
         for _ in range(warmup):
+            flush_l2()
             fn()
         barrier()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
