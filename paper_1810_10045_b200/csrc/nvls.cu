@@ -58,6 +58,10 @@ __device__ __forceinline__ float4 fma4(float s, float4 a, float4 b) {
                      __fmaf_rn(s, a.w, b.w));
 }
 __device__ __forceinline__ float fma4(float s, float a, float b) { return __fmaf_rn(s, a, b); }
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float add4(float a, float b) { return a + b; }
 
 }  // namespace
 
@@ -175,6 +179,68 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
   nv_stamp(a.trace, 52);
 }
 
+// S5+S6 over direct NVLink loads/stores (LSA peer pointers) for small G:
+// rank i owns rows r = i mod G; per owned row it loads the G copies of M[r]
+// (its own and the peers', summed in rank order -- the order of S:142), forms
+// e' = fma(-lr, m, E[I^[r]]) and stores e' into every rank's table window.
+// Per GPU and direction that is (G-1)/G x payload for the loads plus the same
+// for the stores -- 1x at G = 2, where multicast needs (1 + 1/G) = 1.5x.
+template <typename T>
+__global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) {
+  constexpr int W = sizeof(T) / sizeof(float);
+  constexpr int MAXG = 8;
+  ncclCoopCta cta;
+  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
+                                         /*multimem=*/true);
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  const int64_t Ug = a.sc3->u_global;
+  const int C = a.D / W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * NV_WARPS + warp;
+  const int64_t nw = (int64_t)gridDim.x * NV_WARPS;
+  const T* pm[MAXG];
+  T* pe[MAXG];
+#pragma unroll
+  for (int j = 0; j < MAXG; ++j) {
+    pm[j] = j < a.world ? reinterpret_cast<const T*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    pe[j] = j < a.world ? reinterpret_cast<T*>(ncclGetLsaPointer(a.twin, 0, j)) : nullptr;
+  }
+  const T* E = reinterpret_cast<const T*>(a.table);
+  for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
+    const int64_t r = a.rank + a.world * t;
+    const size_t wrow = (size_t)__ldg(a.ihat + r) * C;
+    const size_t mrow = (size_t)r * C;
+    for (int c = lane; c < C; c += 128) {
+      T m[4], e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] = T{};
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if (j < a.world) {
+          T v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            v[q] = (c + 32 * q < C) ? __ldcg(pm[j] + mrow + c + 32 * q) : T{};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) m[q] = j == 0 ? v[q] : add4(m[q], v[q]);  // rank order
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + 32 * q < C) e[q] = fma4(-a.lr, m[q], E[wrow + c + 32 * q]);
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if (j < a.world) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c + 32 * q < C) __stcg(pe[j] + wrow + c + 32 * q, e[q]);
+        }
+      }
+    }
+  }
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
+}
+
 // ---------------------------------------------------------------- host side
 
 struct NvlsState {
@@ -258,12 +324,21 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
   a.world = world;
   const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0;
   static bool once = (max_carveout((const void*)k_nvls_update<float4>),
-                      max_carveout((const void*)k_nvls_update<float>), true);
+                      max_carveout((const void*)k_nvls_update<float>),
+                      max_carveout((const void*)k_p2p_update<float4>),
+                      max_carveout((const void*)k_p2p_update<float>), true);
   (void)once;
-  if (v4)
+  static const int p2p_max = getenv("LMSCALE_P2P_MAX_G") ? atoi(getenv("LMSCALE_P2P_MAX_G")) : 2;
+  if (twin && world <= p2p_max && world <= 8) {
+    if (v4)
+      k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
+    else
+      k_p2p_update<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
+  } else if (v4) {
     k_nvls_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
-  else
+  } else {
     k_nvls_update<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
+  }
 }
 
 }  // namespace lms
