@@ -123,7 +123,8 @@ struct ScatterArgs {
   int2* fixent;           // fix-up entries: (owner chunk, part | nparts << 16)
   float* part2;           // level-2 partial rows, one per entry (fix_cap x D)
   int fix_cap;
-  int zero_rows;          // 0: every slot is present locally (world 1)
+  int zero_rows;          // 0: every slot is present locally (world 1): slot = local index
+  int fill_absent;        // zero the M rows of slots absent on this rank (world > 1)
   int short_runs;         // finish runs <= FX_SHORT in their starting chunk (large K)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
   float lr;
@@ -157,7 +158,10 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st);
 // twin != nullptr: `table` is the symmetric-window table registered as twin.
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
-                        unsigned long long* trace, ncclWindow_t twin, cudaStream_t s);
+                        unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
+                        cudaStream_t s);
+// true: the peer-to-peer fused kernel (presence-aware) is used for this G
+bool nvls_use_p2p(int world);
 ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,
                                  size_t errlen);
 void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w);

@@ -67,6 +67,7 @@ struct lmscale_ctx {
   bool m_nccl = false;
   void* m_reg = nullptr;
   NvlsState* nvls = nullptr;   // fused S5+S6 available
+  size_t lbits_off = 0;        // byte offset of lbits inside the M window
   GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
   float* table_ptr = nullptr;  // lmscale_alloc_table
   size_t table_bytes = 0;
@@ -297,7 +298,8 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fixent = ctx->fixent;
   a.part2 = ctx->part2;
   a.fix_cap = (int)(2 * ctx->nchunks);
-  a.zero_rows = 1;
+  a.zero_rows = ctx->cfg.world > 1 ? 1 : 0;  // world 1: slot = local index
+  a.fill_absent = 1;
   a.short_runs = ctx->last_k >= (1 << 16) ? 1 : 0;
   a.table = nullptr;
   a.lr = 0.f;
@@ -312,11 +314,11 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
 
 // S4 (+ the world-1 S6 when table != nullptr): one cooperative launch.
 lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
-                      float* table = nullptr, float lr = 0.f, bool zero_rows = true) {
+                      float* table = nullptr, float lr = 0.f, bool fill_absent = true) {
   ScatterArgs a = scatter_args(ctx, grad);
   a.table = table;
   a.lr = lr;
-  a.zero_rows = zero_rows ? 1 : 0;
+  a.fill_absent = fill_absent ? 1 : 0;
   CK(launch_scatter(a, s));
   LAUNCHED(1);
   rec(ctx, EV_SCATTER_END, s);
@@ -504,29 +506,37 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       ncclUniqueId id;
       memcpy(&id, nccl_id, sizeof(id));
       NK(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
+      // M and this rank's local presence bitmap share one symmetric window:
+      // the fused kernel reads the peers' bitmaps to load only present rows
+      const size_t lb_off = m_bytes;
+      const size_t win_bytes = align_up(m_bytes + 4 * (size_t)ctx->W, 1 << 21);
       void* m = nullptr;
-      if (ncclMemAlloc(&m, m_bytes) != ncclSuccess)
-        return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(%zu) failed", m_bytes);
+      if (ncclMemAlloc(&m, win_bytes) != ncclSuccess)
+        return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(%zu) failed", win_bytes);
       ctx->M = (float*)m;
       ctx->m_nccl = true;
-      // Fused S5+S6 over NVLS needs a symmetric window with a multicast
-      // mapping; without it, M is registered for NCCL's zero-copy all-reduce.
+      // Fused S5+S6 needs a symmetric window (LSA peer pointers, multicast);
+      // without it, M is registered for NCCL's zero-copy all-reduce.
       char why[256] = {0};
       if (!getenv("LMSCALE_NO_NVLS"))
-        ctx->nvls = nvls_create(ctx->comm, ctx->M, m_bytes, ctx->num_sms, why, sizeof(why));
+        ctx->nvls = nvls_create(ctx->comm, ctx->M, win_bytes, ctx->num_sms, why, sizeof(why));
       else
         snprintf(why, sizeof(why), "LMSCALE_NO_NVLS set");
-      if (!ctx->nvls) {
+      if (ctx->nvls) {
+        ctx->lbits = (uint32_t*)((char*)m + lb_off);
+        ctx->lbits_off = lb_off;
+      } else {
         snprintf(ctx->nvls_why, sizeof(ctx->nvls_why), "%s", why);
-        NK(ncclCommRegister(ctx->comm, ctx->M, m_bytes, &ctx->m_reg));
+        NK(ncclCommRegister(ctx->comm, ctx->M, win_bytes, &ctx->m_reg));
       }
+      CK(cudaMemset(m, 0, win_bytes));
     } else {
       if (cudaMalloc((void**)&ctx->M, m_bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(%zu) failed", m_bytes);
       }
     }
-    CK(cudaMemset(ctx->M, 0, m_bytes));
+    if (!ctx->m_nccl) CK(cudaMemset(ctx->M, 0, m_bytes));
     off += m_bytes;
     if (getenv("LMSCALE_PHASE_TRACE")) {
       CK(cudaMalloc(&ctx->trace, 64 * sizeof(unsigned long long)));
@@ -743,14 +753,17 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   // (fusing S6 into S4's cooperative kernel at world 1 was measured slower
   // than the separate, higher-occupancy update launch; kept separate)
   const bool fuse_s6 = false;
-  st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*zero_rows=*/G > 1);
+  // the peer-to-peer fused kernel loads only present rows: no zero-fill of M
+  const bool p2p = G > 1 && table && ctx->nvls && table == ctx->table_ptr && ctx->table_win &&
+                   nvls_use_p2p(G);
+  st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*fill_absent=*/G > 1 && !p2p);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
   if (G > 1 && table && ctx->nvls) {
     // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
                        ctx->cfg.rank, G, ctx->trace,
-                       table == ctx->table_ptr ? ctx->table_win : nullptr, s);
+                       table == ctx->table_ptr ? ctx->table_win : nullptr, ctx->lbits_off, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {

@@ -77,6 +77,7 @@ struct NvlsKernelArgs {
   int rank, world;
   unsigned long long* trace;
   int diag;  // timing diagnostics only (LMSCALE_NVLS_DIAG): 1 no broadcast, 2 no reduce
+  size_t lbits_off;  // byte offset of each rank's local presence bitmap in the M window
   ncclWindow_t twin;  // non-null: the table is in a symmetric window; updated rows are
                       // multicast straight into every replica of E (no copy phase)
 };
@@ -205,24 +206,38 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
     pm[j] = j < a.world ? reinterpret_cast<const T*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
     pe[j] = j < a.world ? reinterpret_cast<T*>(ncclGetLsaPointer(a.twin, 0, j)) : nullptr;
   }
+  const uint32_t* pb[MAXG];  // each rank's local presence bitmap (S1's lbits)
+#pragma unroll
+  for (int j = 0; j < MAXG; ++j)
+    pb[j] = j < a.world ? reinterpret_cast<const uint32_t*>(
+                              reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j)) +
+                              a.lbits_off)
+                        : nullptr;
   const T* E = reinterpret_cast<const T*>(a.table);
   for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
     const int64_t r = a.rank + a.world * t;
-    const size_t wrow = (size_t)__ldg(a.ihat + r) * C;
+    const uint32_t w = __ldg(a.ihat + r);
+    const size_t wrow = (size_t)w * C;
     const size_t mrow = (size_t)r * C;
+    // which ranks hold word w: only their copies of M[r] are loaded (absent
+    // ranks' rows are never written: S4 skips the zero-fill on this path)
+    uint32_t has = 0;
+#pragma unroll
+    for (int j = 0; j < MAXG; ++j)
+      if (j < a.world) has |= ((__ldcg(pb[j] + (w >> 5)) >> (w & 31u)) & 1u) << j;
     for (int c = lane; c < C; c += 128) {
       T m[4], e[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) m[q] = T{};
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
-        if (j < a.world) {
+        if ((has >> j) & 1u) {
           T v[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             v[q] = (c + 32 * q < C) ? __ldcg(pm[j] + mrow + c + 32 * q) : T{};
 #pragma unroll
-          for (int q = 0; q < 4; ++q) m[q] = j == 0 ? v[q] : add4(m[q], v[q]);  // rank order
+          for (int q = 0; q < 4; ++q) m[q] = add4(m[q], v[q]);  // rank order
         }
       }
 #pragma unroll
@@ -289,6 +304,12 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st) {
   delete st;
 }
 
+bool nvls_use_p2p(int world) {
+  static const int p2p_max =
+      getenv("LMSCALE_P2P_MAX_G") ? atoi(getenv("LMSCALE_P2P_MAX_G")) : 8;
+  return world <= p2p_max && world <= 8;
+}
+
 ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,
                                  size_t errlen) {
   ncclWindow_t w = nullptr;
@@ -306,8 +327,10 @@ void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w) {
 
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
-                        unsigned long long* trace, ncclWindow_t twin, cudaStream_t s) {
+                        unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
+                        cudaStream_t s) {
   NvlsKernelArgs a;
+  a.lbits_off = lbits_off;
   a.twin = twin;
   a.trace = trace;
   static const int diag = getenv("LMSCALE_NVLS_DIAG") ? atoi(getenv("LMSCALE_NVLS_DIAG")) : 0;
@@ -328,8 +351,7 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
                       max_carveout((const void*)k_p2p_update<float4>),
                       max_carveout((const void*)k_p2p_update<float>), true);
   (void)once;
-  static const int p2p_max = getenv("LMSCALE_P2P_MAX_G") ? atoi(getenv("LMSCALE_P2P_MAX_G")) : 2;
-  if (twin && world <= p2p_max && world <= 8) {
+  if (twin && nvls_use_p2p(world)) {
     if (v4)
       k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
     else

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
   const int nchunks = (K + SC_CHUNK - 1) / SC_CHUNK;
   const int64_t Ug = a.sc3->u_global;
-  const int64_t nz = a.zero_rows ? (Ug + SC_ZGROUP - 1) / SC_ZGROUP : 0;
+  const int64_t nz = a.zero_rows && a.fill_absent ? (Ug + SC_ZGROUP - 1) / SC_ZGROUP : 0;
   const int64_t items = ((int64_t)nchunks + nz) * ncb;
   const int lane = (int)lane_id();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -398,7 +398,7 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   const int C = a.D / Vec<T>::W;
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
   const int64_t nchunks = (a.K + SC_CHUNK - 1) / SC_CHUNK;
-  const int64_t nz = a.zero_rows ? (a.ug_cap + SC_ZGROUP - 1) / SC_ZGROUP : 0;
+  const int64_t nz = a.zero_rows && a.fill_absent ? (a.ug_cap + SC_ZGROUP - 1) / SC_ZGROUP : 0;
   int64_t blocks = ((nchunks + nz) * ncb * 32 + SC_THREADS - 1) / SC_THREADS;
   const int64_t cap = (int64_t)a.num_sms * occ;
   if (blocks > cap) blocks = cap;
