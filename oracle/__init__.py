@@ -74,6 +74,12 @@ def _load():
             lib.oracle_sync_dense.argtypes = [P, P, i64, i64, ctypes.c_int, P, P, P,
                                               ctypes.c_double]
             lib.oracle_type_gradient.restype = i64
+            lib.oracle_compress.restype = None
+            lib.oracle_compress.argtypes = [P, i64, ctypes.c_float, P]
+            lib.oracle_decompress.restype = None
+            lib.oracle_decompress.argtypes = [P, i64, ctypes.c_float, P]
+            lib.oracle_sum_f32.restype = None
+            lib.oracle_sum_f32.argtypes = [P, ctypes.c_int, i64, P]
             lib.oracle_type_gradient.argtypes = [P, P, P, ctypes.c_int, i64,
                                                  ctypes.c_uint32, P, P]
             _lib = lib
@@ -211,6 +217,71 @@ def sync_unique(J_list, delta_list, E, lr):
     update_rows(E, Ihat, Mhat64, lr)                     # step 7
     return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M=Ms,
                 Mhat64=Mhat64, Mhat=Mhat64.astype(np.float32), E=E)
+
+
+def compress(x, F):
+    """Sec. 3.3: binary16 bits (uint16) of RNE(fp32(F * x)),
+    saturated to +-65504 (R15)."""
+    lib = _load()
+    x = _f32(x)
+    q = np.empty(x.shape, np.uint16)
+    lib.oracle_compress(_p(x), x.size, float(F), _p(q))
+    return q
+
+
+def decompress(q, F):
+    """Sec. 3.3 (P:511): fp32(half) / F."""
+    lib = _load()
+    q = np.ascontiguousarray(q, dtype=np.uint16)
+    x = np.empty(q.shape, np.float32)
+    lib.oracle_decompress(_p(q), q.size, float(F), _p(x))
+    return x
+
+
+def sum_f32(a_list):
+    """Rank-ordered fp32 sum of the up-cast payloads (R15)."""
+    lib = _load()
+    As = [_f32(a) for a in a_list]
+    out = np.empty_like(As[0])
+    lib.oracle_sum_f32(_ptr_array(As), len(As), out.size, _p(out))
+    return out
+
+
+def sync_unique_compressed(J_list, delta_list, E, lr, F):
+    """The uniqueness exchange with compression (Sec. 3.3 on Sec. 3.1).
+
+    Steps 1-5 as ``sync_unique``; each M_i is an FP32 tensor, so it is
+    rounded once to fp32.  Step 6, the all-reduce, runs as the two exchanges
+    of a reduce-scatter + all-gather, each with the paper's codec (R15):
+
+    a. every rank sends compress(M_i, F); the receiver up-casts, divides by F
+       and sums in fp32, rank order -> S;
+    b. S is sent as compress(S, F) and every rank up-casts and divides:
+       M^ = decompress(compress(S, F), F).
+
+    Step 7 is ``update_rows`` with that M^.  E is updated in place.
+    """
+    G = len(J_list)
+    ranks = []
+    for g in range(G):                                   # steps 1, 2
+        Jhat, counts, inverse = unique_local(J_list[g])
+        dhat = reduce_local(delta_list[g], inverse, Jhat.size)
+        ranks.append(dict(Jhat=Jhat, counts=counts, inverse=inverse, dhat=dhat))
+    I = allgather_ids(J_list)                            # step 3
+    Ihat, gcounts = unique_global(I)                     # step 4
+    Ug = Ihat.size
+    M32, Q = [], []
+    for r in ranks:
+        r["l2g"], r["slot"] = remap(r["Jhat"], Ihat, r["inverse"])
+        m = scatter_expand(r["dhat"], r["l2g"], Ug).astype(np.float32)   # step 5
+        M32.append(m)
+        Q.append(compress(m, F))                         # 6a: down-cast on the sender
+    S = sum_f32([decompress(q, F) for q in Q])           # 6a: up-cast, sum (receiver)
+    Qhat = compress(S, F)                                # 6b: the reduced rows, down-cast
+    Mhat = decompress(Qhat, F)                           # 6b: up-cast on every rank
+    update_rows(E, Ihat, Mhat.astype(np.float64), lr)    # step 7
+    return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M32=M32, Q=Q, S=S,
+                Qhat=Qhat, Mhat=Mhat, E=E)
 
 
 def sync_dense(J_list, delta_list, E, lr):

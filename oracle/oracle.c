@@ -213,3 +213,48 @@ int64_t oracle_type_gradient(const uint32_t* const* J, const float* const* delta
       }
   return n;
 }
+
+/*
+ * Compression (Sec. 3.3): "multiply the FP32 tensor by a scaling
+ * factor, F before down-casting" to FP16.  Reading R15: the product F*x is an
+ * fp32 product (the tensor is FP32), the down-cast is IEEE binary16
+ * round-to-nearest-even (through subnormals to +-0), and values beyond the
+ * largest finite half saturate to +-65504.  q holds the binary16 bits.
+ * The conversion is the compiler's _Float16 cast (IEEE RNE): a primitive.
+ */
+void oracle_compress(const float* x, int64_t n, float F, uint16_t* q) {
+  for (int64_t i = 0; i < n; ++i) {
+    float p = F * x[i];
+    _Float16 h;
+    if (p > 65504.0f)
+      h = (_Float16)65504.0f;
+    else if (p < -65504.0f)
+      h = (_Float16)-65504.0f;
+    else
+      h = (_Float16)p;
+    memcpy(q + i, &h, sizeof(h));
+  }
+}
+
+/*
+ * "up-cast the FP16 tensor to FP32 at the receiving end" and "divide again by
+ * F after up-casting": x = fp32(half) / F, one fp32 division.
+ */
+void oracle_decompress(const uint16_t* q, int64_t n, float F, float* x) {
+  for (int64_t i = 0; i < n; ++i) {
+    _Float16 h;
+    memcpy(&h, q + i, sizeof(h));
+    x[i] = (float)h / F;
+  }
+}
+
+/*
+ * The receiving end's reduction with compression on (R15): the up-cast
+ * tensors are FP32, so the sum over ranks is an fp32 sum, in rank
+ * order.  out has n entries, overwritten.
+ */
+void oracle_sum_f32(const float* const* a, int G, int64_t n, float* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = 0.0f;
+  for (int g = 0; g < G; ++g)
+    for (int64_t i = 0; i < n; ++i) out[i] += a[g][i];
+}
