@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches (no CUDA graph)")
+    ap.add_argument("--compress", type=float, default=0.0,
+                    help="Sec. 3.3 compressed exchange with scale F (0 = off, fp32 rows)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
@@ -178,7 +180,8 @@ def config_dict(cfg, args, world):
             "parallelism": f"dp{world}",
             "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read sweep), "
                   "outside the timed region",
-            "cuda_graph": not getattr(args, "no_graph", True)}
+            "cuda_graph": not getattr(args, "no_graph", True),
+            "compression": f"fp16:F={args.compress:g}" if args.compress > 0 else "off"}
 
 
 def emit(line, args):
@@ -248,6 +251,8 @@ def main():
         table.copy_(synth.table_values(cfg.V, cfg.D, args.mode, device=dev))
     else:
         table = synth.table_values(cfg.V, cfg.D, args.mode, device=dev)
+    if args.compress > 0:
+        ctx.set_compression(args.compress)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 
@@ -380,9 +385,31 @@ def main():
                            "the kernel on its launch stream; that pass's step time: "
                            f"{max_over_ranks(sum(ms_s4), dev) / args.steps * 1e3:.1f} us")
     roof["traffic"] = ncu_traffic(cfg.name, world)
-    if st_last.get("fused_s5_s6"):
-        nvl = (1 + 1 / world) * 4 * ug * D   # bytes per direction per GPU
-        upd = {"kernel": "k_nvls_update (S5+S6 fused, NVLS multimem)", "bound": "nvlink",
+    fused = st_last.get("fused_s5_s6", 0)
+    if fused:
+        # NVLink ingress per GPU (the busier direction), averaged over ranks:
+        #   P2P kernels: owners load the remote present copies of their rows
+        #   (sum_i U_i (G-1)/G^2 rows) and receive the other owners' rows
+        #   ((G-1)/G U_g rows); 4 B/elem fp32, 2 B/elem compressed (R15);
+        #   NVLS multicast: (1 + 1/G) U_g rows (reduce + broadcast).
+        if dist.is_initialized():
+            t = torch.tensor([float(info.get("u_local") or 0)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t)
+            ui_sum = float(t.item())
+        else:
+            ui_sum = float(info.get("u_local") or 0)
+        p2p = fused == 3 or (fused == 2 and world <= 8)
+        esz = 2 if fused == 3 else 4
+        if p2p:
+            rows_in = ui_sum * (world - 1) / world ** 2 + ug * (world - 1) / world
+            kname2 = ("k_p2p_update_c (compressed S5+S6: binary16 reduce-scatter + all-gather "
+                      "over NVLink P2P, local S6)" if fused == 3 else
+                      "k_p2p_update (S5+S6 fused over NVLink P2P: present rows only)")
+        else:
+            rows_in = (1 + 1 / world) * ug
+            kname2 = "k_nvls_update (S5+S6 fused, NVLS multimem)"
+        nvl = rows_in * esz * D
+        upd = {"kernel": kname2, "bound": "nvlink",
                "bytes_per_direction": nvl, "us_per_launch": ph["us_allreduce"],
                "achieved": nvl / (ph["us_allreduce"] * 1e-6) / 1e9, "peak": 770.0,
                "peak_kind": "guide: measured peer copy per direction (900 nominal)"}

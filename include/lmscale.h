@@ -108,7 +108,9 @@ typedef struct {
   int32_t kernels_total_lo;    /* running count of launched kernels (low 31 bits) */
   int32_t fused_s5_s6;         /* 1: the last step ran S5+S6 as one NVLS multicast kernel
                                   (us_allreduce then times that kernel, us_update ~ 0);
-                                  2: same, multicasting straight into the table windows */
+                                  2: same, multicasting straight into the table windows;
+                                  3: the compressed (binary16) exchange of
+                                  lmscale_set_compression */
   int32_t nvls_available;      /* 1: the context has the multicast window (world > 1) */
 } lmscale_stats;
 
@@ -250,6 +252,32 @@ LMSCALE_API lmscale_status lmscale_alloc_table(lmscale_ctx* ctx, float** table_o
  * GPU-side serialisation point of a few microseconds, so mode 2 inflates the
  * step it measures).  FLAG_TIMING at init selects mode 2. */
 LMSCALE_API lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode);
+
+/* Compression (Sec. 3.3; reading R15).  F > 0 makes
+ * every later collective lmscale_step / lmscale_train_step_host (world > 1)
+ * exchange binary16 payloads instead of fp32 rows:
+ *   - S4 stores each row of M_g as RNE(fp32(F * x)), saturated to +-65504;
+ *   - the owner of row r (r mod world == rank) up-casts the copies of the ranks
+ *     holding word I^[r], divides each by F, sums them in fp32 in rank order
+ *     and sends the compressed sum to every rank;
+ *   - every rank up-casts M^ (one fp32 division by F) and applies S6 to its
+ *     own table: E[I^[r]] = fma(-lr, M^[r], E[I^[r]]).
+ * Half the NVLink bytes of the fp32 exchange; replicas stay bit-identical.
+ * F == 0 turns compression off.  F < 0 or non-finite: INVALID_ARG.  world > 1
+ * needs the symmetric window (stats.nvls_available == 1), else UNSUPPORTED.
+ * world == 1 has no communication and is unaffected.  While compression is
+ * on, lmscale_sync_embedding_grad (fp32 M^ rows through NCCL) returns
+ * UNSUPPORTED. */
+LMSCALE_API lmscale_status lmscale_set_compression(lmscale_ctx* ctx, float F);
+
+/* The codec alone, device pointers, stream-ordered, i < n:
+ * compress:   q[i] = binary16 bits of RNE(fp32(F * x[i])), saturated to +-65504;
+ * decompress: x[i] = fp32(q[i]) / F (exact widening, one fp32 division).
+ * F > 0 and finite, n >= 0 (n == 0 launches nothing), else INVALID_ARG. */
+LMSCALE_API lmscale_status lmscale_compress(lmscale_ctx* ctx, const float* x, int64_t n, float F,
+                                            uint16_t* q, void* stream);
+LMSCALE_API lmscale_status lmscale_decompress(lmscale_ctx* ctx, const uint16_t* q, int64_t n,
+                                              float F, float* x, void* stream);
 
 LMSCALE_API lmscale_status lmscale_get_stats(const lmscale_ctx* ctx, lmscale_stats* out /* host */);
 LMSCALE_API const char* lmscale_status_string(lmscale_status s);

@@ -1,6 +1,7 @@
 // common.cuh -- device helpers shared by the lmscale kernels (sm_100a).
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -142,6 +143,29 @@ __device__ __forceinline__ void grid_barrier(GridBar* b) {
 inline void max_carveout(const void* f) {
   static const bool off = getenv("LMSCALE_NO_CARVEOUT") != nullptr;
   if (!off) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+// ---- compression codec (Sec. 3.3; R15) -------------
+// down-cast: binary16 round-to-nearest-even of the fp32 product F * x,
+// saturated to +-65504; up-cast: exact widening, then one fp32 division by F.
+__device__ __forceinline__ __half enc1(float x, float F) {
+  return __float2half_rn(fminf(fmaxf(__fmul_rn(F, x), -65504.f), 65504.f));
+}
+__device__ __forceinline__ uint32_t enc2(float x, float y, float F) {
+  const __half2 h = __halves2half2(enc1(x, F), enc1(y, F));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float dec1(__half h, float F) { return __fdiv_rn(__half2float(h), F); }
+__device__ __forceinline__ float2 dec2(uint32_t u, float F) {
+  const __half2 h = *reinterpret_cast<const __half2*>(&u);
+  return make_float2(dec1(__low2half(h), F), dec1(__high2half(h), F));
+}
+__device__ __forceinline__ uint2 enc4(float4 v, float F) {
+  return make_uint2(enc2(v.x, v.y, F), enc2(v.z, v.w, F));
+}
+__device__ __forceinline__ float4 dec4(uint2 u, float F) {
+  const float2 a = dec2(u.x, F), b = dec2(u.y, F);
+  return make_float4(a.x, a.y, b.x, b.y);
 }
 
 }  // namespace lms

@@ -125,6 +125,8 @@ struct ScatterArgs {
   int fix_cap;
   int zero_rows;          // 0: every slot is present locally (world 1): slot = local index
   int fill_absent;        // zero the M rows of slots absent on this rank (world > 1)
+  int m16;                // M rows are stored compressed (binary16 of cF * x, R15)
+  float cF;               // compression scale F
   int short_runs;         // finish runs <= FX_SHORT in their starting chunk (large K)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
   float lr;
@@ -139,6 +141,9 @@ struct ScatterArgs {
 };
 // One cooperative launch: scatter, cut-run fixup, and (a.table) the world-1 S6.
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
+// compression codec (R15): down = compress (fp32 -> binary16 bits), else decompress
+cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* out, int num_sms,
+                         cudaStream_t s);
 
 // ---- S6 / S0 --------------------------------------------------------------
 // n_dev != nullptr: the row count is read on the device (min(n, *n_dev)); n
@@ -159,7 +164,7 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st);
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
-                        cudaStream_t s);
+                        float cF, size_t mhat_off, cudaStream_t s);
 // true: the peer-to-peer fused kernel (presence-aware) is used for this G
 bool nvls_use_p2p(int world);
 ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,

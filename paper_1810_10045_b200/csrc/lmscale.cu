@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -68,6 +69,8 @@ struct lmscale_ctx {
   void* m_reg = nullptr;
   NvlsState* nvls = nullptr;   // fused S5+S6 available
   size_t lbits_off = 0;        // byte offset of lbits inside the M window
+  size_t mhat_off = 0;         // byte offset of the compressed M^ rows inside the M window
+  float cF = 0.f;              // compression scale (0: off), lmscale_set_compression
   GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
   float* table_ptr = nullptr;  // lmscale_alloc_table
   size_t table_bytes = 0;
@@ -300,6 +303,8 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fix_cap = (int)(2 * ctx->nchunks);
   a.zero_rows = ctx->cfg.world > 1 ? 1 : 0;  // world 1: slot = local index
   a.fill_absent = 1;
+  a.m16 = 0;
+  a.cF = 0.f;
   a.short_runs = ctx->last_k >= (1 << 16) ? 1 : 0;
   a.table = nullptr;
   a.lr = 0.f;
@@ -314,11 +319,14 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
 
 // S4 (+ the world-1 S6 when table != nullptr): one cooperative launch.
 lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
-                      float* table = nullptr, float lr = 0.f, bool fill_absent = true) {
+                      float* table = nullptr, float lr = 0.f, bool fill_absent = true,
+                      float m16_F = 0.f) {
   ScatterArgs a = scatter_args(ctx, grad);
   a.table = table;
   a.lr = lr;
   a.fill_absent = fill_absent ? 1 : 0;
+  a.m16 = m16_F > 0.f ? 1 : 0;
+  a.cF = m16_F;
   CK(launch_scatter(a, s));
   LAUNCHED(1);
   rec(ctx, EV_SCATTER_END, s);
@@ -389,6 +397,44 @@ lmscale_status lmscale_alloc_table(lmscale_ctx* ctx, float** table_out, int64_t*
   return LMSCALE_OK;
 }
 
+lmscale_status lmscale_set_compression(lmscale_ctx* ctx, float F) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!(F >= 0.f) || std::isinf(F))
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "compression scale F=%g must be >= 0 and finite", F);
+  if (F > 0.f && comm_enabled(ctx) && !ctx->nvls)
+    return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "compression needs the symmetric window: %s",
+                ctx->nvls_why);
+  if (F > 0.f && (ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
+    return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "compression on a NO_COMM context");
+  ctx->cF = F;
+  return LMSCALE_OK;
+}
+
+static lmscale_status codec_call(lmscale_ctx* ctx, bool down, const void* in, int64_t n, float F,
+                                 void* out, void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (n < 0 || !(F > 0.f) || std::isinf(F))
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "codec: n=%lld F=%g", (long long)n, F);
+  if (n == 0) return LMSCALE_OK;
+  if (!in || !out) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "codec: NULL pointer");
+  cudaSetDevice(ctx->cfg.device);
+  begin_call(ctx);
+  CK(launch_codec(down, in, n, F, out, ctx->num_sms, S(stream)));
+  LAUNCHED(1);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_compress(lmscale_ctx* ctx, const float* x, int64_t n, float F, uint16_t* q,
+                                void* stream) {
+  return codec_call(ctx, true, x, n, F, q, stream);
+}
+
+lmscale_status lmscale_decompress(lmscale_ctx* ctx, const uint16_t* q, int64_t n, float F, float* x,
+                                  void* stream) {
+  return codec_call(ctx, false, q, n, F, x, stream);
+}
+
 lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return LMSCALE_ERR_INVALID_ARG;
   if (mode != ctx->tmode && ctx->gexec) {  // the captured graph carries the old events
@@ -454,7 +500,9 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W);
     // M lives in its own allocation: with a communicator it comes from
     // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
-    const size_t m_bytes = align_up(4 * (size_t)ctx->ucap * D, 1 << 21);
+    // (+256: room to align the compressed M^ region at byte 2*ucap*D)
+    const size_t m_bytes = align_up(4 * (size_t)ctx->ucap * D + 256, 1 << 21);
+    ctx->mhat_off = align_up(2 * (size_t)ctx->ucap * D, 256);
     size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
     size_t o_part2 = take(4 * (size_t)2 * ctx->nchunks * D);
     ctx->ws_bytes = off;
@@ -699,6 +747,9 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   if (!grad) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "grad is NULL");
   if ((ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
     return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "collective call on a NO_COMM context");
+  if (ctx->cF > 0.f && ctx->cfg.world > 1 && !table)
+    return fail(ctx, LMSCALE_ERR_UNSUPPORTED,
+                "compression is on: the compressed exchange runs in lmscale_step (with a table)");
   begin_call(ctx);
   cudaStream_t s = S(stream);
   const int G = ctx->cfg.world;
@@ -754,16 +805,20 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   // than the separate, higher-occupancy update launch; kept separate)
   const bool fuse_s6 = false;
   // the peer-to-peer fused kernel loads only present rows: no zero-fill of M
-  const bool p2p = G > 1 && table && ctx->nvls && table == ctx->table_ptr && ctx->table_win &&
-                   nvls_use_p2p(G);
-  st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*fill_absent=*/G > 1 && !p2p);
+  // compressed exchange (R15): S4 writes binary16 rows, present rows only
+  const bool comp = G > 1 && ctx->cF > 0.f;
+  const bool p2p = G > 1 && table && ctx->nvls &&
+                   (comp || (table == ctx->table_ptr && ctx->table_win && nvls_use_p2p(G)));
+  st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*fill_absent=*/G > 1 && !p2p,
+              comp ? ctx->cF : 0.f);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
   if (G > 1 && table && ctx->nvls) {
     // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
                        ctx->cfg.rank, G, ctx->trace,
-                       table == ctx->table_ptr ? ctx->table_win : nullptr, ctx->lbits_off, s);
+                       table == ctx->table_ptr ? ctx->table_win : nullptr, ctx->lbits_off,
+                       comp ? ctx->cF : 0.f, ctx->mhat_off, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {
@@ -780,7 +835,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
-    ctx->fused_last = (table == ctx->table_ptr && ctx->table_win) ? 2 : 1;
+    ctx->fused_last = comp ? 3 : (table == ctx->table_ptr && ctx->table_win) ? 2 : 1;
     int64_t ug = -1;
     if (need_host_ug) {
       CK(cudaEventSynchronize(ctx->ev_copy));

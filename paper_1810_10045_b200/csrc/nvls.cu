@@ -21,6 +21,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -62,6 +63,10 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 __device__ __forceinline__ float add4(float a, float b) { return a + b; }
+__device__ __forceinline__ float4 dech(uint2 u, float F) { return dec4(u, F); }
+__device__ __forceinline__ float dech(__half h, float F) { return dec1(h, F); }
+__device__ __forceinline__ uint2 ench(float4 v, float F) { return enc4(v, F); }
+__device__ __forceinline__ __half ench(float v, float F) { return enc1(v, F); }
 
 }  // namespace
 
@@ -80,6 +85,8 @@ struct NvlsKernelArgs {
   size_t lbits_off;  // byte offset of each rank's local presence bitmap in the M window
   ncclWindow_t twin;  // non-null: the table is in a symmetric window; updated rows are
                       // multicast straight into every replica of E (no copy phase)
+  float cF;           // compression scale F (k_p2p_update_c)
+  size_t mhat_off;    // byte offset of the compressed M^ rows in the M window
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -256,6 +263,105 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
   bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
 }
 
+
+// Compressed S5+S6 (Sec. 3.3; R15): the all-reduce as a
+// reduce-scatter and an all-gather, each carrying binary16 payloads.
+//   1. LSA barrier: every rank's compressed M_g (written by S4) is complete;
+//   2. rank i owns rows r = i mod G: it loads the copies of the ranks that hold
+//      word I^[r] (peers' presence bitmaps), up-casts, divides by F, sums in
+//      fp32 in rank order, compresses the sum and stores it into every rank's
+//      M^ region (P2P stores, half the bytes of fp32 rows);
+//   3. LSA barrier: every compressed row of M^ has landed;
+//   4. every rank updates all U_g rows of its own E from its local M^:
+//      E[I^[r]] = fma(-lr, dec(M^[r]), E[I^[r]]) -- the same instruction on the
+//      same bits on every rank, so the replicas stay bit-identical.
+// Per GPU and direction: (G-1)/G x (present rows + U_g rows) x 2 bytes x D.
+template <typename T>
+__global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a) {
+  constexpr int W = sizeof(T) / sizeof(float);
+  using H = typename std::conditional<W == 4, uint2, __half>::type;
+  constexpr int MAXG = 8;
+  ncclCoopCta cta;
+  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
+                                         /*multimem=*/true);
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's compressed M_g is complete
+  const int64_t Ug = a.sc3->u_global;
+  const int C = a.D / W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * NV_WARPS + warp;
+  const int64_t nw = (int64_t)gridDim.x * NV_WARPS;
+  const float F = a.cF;
+  const H* pm[MAXG];
+  H* pq[MAXG];
+  const uint32_t* pb[MAXG];
+#pragma unroll
+  for (int j = 0; j < MAXG; ++j) {
+    char* base = j < a.world ? reinterpret_cast<char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    pm[j] = reinterpret_cast<const H*>(base);
+    pq[j] = reinterpret_cast<H*>(base + a.mhat_off);
+    pb[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
+  }
+  for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
+    const int64_t r = a.rank + a.world * t;
+    const uint32_t w = __ldg(a.ihat + r);
+    const size_t mrow = (size_t)r * C;
+    uint32_t has = 0;
+#pragma unroll
+    for (int j = 0; j < MAXG; ++j)
+      if (j < a.world) has |= ((__ldcg(pb[j] + (w >> 5)) >> (w & 31u)) & 1u) << j;
+    for (int c = lane; c < C; c += 128) {
+      T m[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] = T{};
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if ((has >> j) & 1u) {
+          H v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c + 32 * q < C) v[q] = pm[j][mrow + c + 32 * q];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c + 32 * q < C) m[q] = add4(m[q], dech(v[q], F));  // rank order, fp32
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (c + 32 * q < C) {
+          const H e = ench(m[q], F);
+#pragma unroll
+          for (int j = 0; j < MAXG; ++j)
+            if (j < a.world) pq[j][mrow + c + 32 * q] = e;
+        }
+      }
+    }
+  }
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every compressed row of M^ has landed
+  const H* Q = reinterpret_cast<const H*>(reinterpret_cast<const char*>(a.M) + a.mhat_off);
+  T* E = reinterpret_cast<T*>(a.table);
+  // rows in the same (owner, t) order as phase 1: the barrier above is per
+  // CTA index, so CTA k may only read the rows that CTAs k wrote
+  for (int j = 0; j < a.world; ++j)
+  for (int64_t t = gw; j + a.world * t < Ug; t += nw) {
+    const int64_t r = j + a.world * t;
+    T* er = E + (size_t)__ldg(a.ihat + r) * C;
+    const H* qr = Q + (size_t)r * C;
+    for (int c = lane; c < C; c += 128) {
+      H v[4];
+      T e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + 32 * q < C) {
+          v[q] = __ldcg(qr + c + 32 * q);
+          e[q] = er[c + 32 * q];
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + 32 * q < C) er[c + 32 * q] = fma4(-a.lr, dech(v[q], F), e[q]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 struct NvlsState {
@@ -328,9 +434,11 @@ void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w) {
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
-                        cudaStream_t s) {
+                        float cF, size_t mhat_off, cudaStream_t s) {
   NvlsKernelArgs a;
   a.lbits_off = lbits_off;
+  a.cF = cF;
+  a.mhat_off = mhat_off;
   a.twin = twin;
   a.trace = trace;
   static const int diag = getenv("LMSCALE_NVLS_DIAG") ? atoi(getenv("LMSCALE_NVLS_DIAG")) : 0;
@@ -349,9 +457,16 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
   static bool once = (max_carveout((const void*)k_nvls_update<float4>),
                       max_carveout((const void*)k_nvls_update<float>),
                       max_carveout((const void*)k_p2p_update<float4>),
-                      max_carveout((const void*)k_p2p_update<float>), true);
+                      max_carveout((const void*)k_p2p_update<float>),
+                      max_carveout((const void*)k_p2p_update_c<float4>),
+                      max_carveout((const void*)k_p2p_update_c<float>), true);
   (void)once;
-  if (twin && nvls_use_p2p(world)) {
+  if (cF > 0.f) {  // compressed exchange (any table; G <= 8)
+    if (v4)
+      k_p2p_update_c<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
+    else
+      k_p2p_update_c<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
+  } else if (twin && nvls_use_p2p(world)) {
     if (v4)
       k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
     else

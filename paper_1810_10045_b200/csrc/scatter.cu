@@ -55,6 +55,22 @@ struct Vec<float> {
 constexpr int SC_THREADS = 256;
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
+// Store element block `col` of M row `slot`: fp32, or compressed binary16
+// (the payload of the compressed exchange) when a.m16.
+__device__ __forceinline__ void st_m(const ScatterArgs& a, size_t slot, int C, int col, float4 v) {
+  if (a.m16) {
+    reinterpret_cast<uint2*>(a.M)[slot * C + col] = enc4(v, a.cF);
+  } else {
+    st_v4(reinterpret_cast<float4*>(a.M) + slot * C + col, v);
+  }
+}
+__device__ __forceinline__ void st_m(const ScatterArgs& a, size_t slot, int C, int col, float v) {
+  if (a.m16)
+    reinterpret_cast<__half*>(a.M)[slot * C + col] = enc1(v, a.cF);
+  else
+    a.M[slot * C + col] = v;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------- S4
@@ -158,7 +174,14 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
                 if (ent + j < a.fix_cap) a.fixent[ent + j] = make_int2(c, j | (nparts << 16));
             }
           } else {
-            dst = slot >= 0 ? M + (size_t)slot * C : nullptr;
+            dst = nullptr;
+            if (slot >= 0) {
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                const int col = col0 + v * 32;
+                if (FULLC || col < C) st_m(a, (size_t)slot, C, col, acc[v]);
+              }
+            }
           }
           if (dst) {
 #pragma unroll
@@ -222,21 +245,21 @@ __device__ __forceinline__ void fixup_part(const ScatterArgs& a, T (*red)[32 * N
   for (int v = 0; v < NV; ++v) red[warp][v * 32 + lane] = acc[v];
   __syncthreads();
   if (warp == 0) {
-    T* dst;
-    if (nparts == 1) {
-      const int slot = a.zero_rows ? __ldcg(a.l2g + u) : u;
-      dst = slot >= 0 ? reinterpret_cast<T*>(a.M) + (size_t)slot * C : nullptr;
-    } else {
-      dst = reinterpret_cast<T*>(a.part2) + (size_t)e * C;
-    }
-    if (dst) {
+    const int slot = nparts == 1 ? (a.zero_rows ? __ldcg(a.l2g + u) : u) : -1;
+    T* dst = nparts == 1 ? nullptr : reinterpret_cast<T*>(a.part2) + (size_t)e * C;
+    if (dst || slot >= 0) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         T sum = red[0][v * 32 + lane];
 #pragma unroll
         for (int w = 1; w < NWF; ++w) sum = V::add(sum, red[w][v * 32 + lane]);
         const int col = col0 + v * 32;
-        if (col < C) V::st(dst + col, sum);
+        if (col < C) {
+          if (dst)
+            V::st(dst + col, sum);
+          else
+            st_m(a, (size_t)slot, C, col, sum);
+        }
       }
     }
   }
@@ -263,7 +286,7 @@ __device__ __forceinline__ void fixup_final(const ScatterArgs& a, int e0, int cb
     if (col >= C) continue;
     T sum = V::ld_l2(L2 + (size_t)e0 * C + col);
     for (int j = 1; j < nparts; ++j) sum = V::add(sum, V::ld_l2(L2 + (size_t)(e0 + j) * C + col));
-    V::st(reinterpret_cast<T*>(a.M) + (size_t)slot * C + col, sum);
+    st_m(a, (size_t)slot, C, col, sum);
   }
 }
 
@@ -324,11 +347,10 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
       while (am) {
         const int b = __ffs(am) - 1;
         am &= am - 1;
-        T* dst = M + (size_t)(r0 + b) * C;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int col = col0 + v * 32;
-          if (col < C) V::st(dst + col, V::zero());
+          if (col < C) st_m(a, (size_t)(r0 + b), C, col, V::zero());
         }
       }
     }
@@ -519,4 +541,34 @@ void launch_dense(float* table, int D, const uint32_t* ids, const float* grad, i
     k_dense_s<<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, grad, n, lr, vocab);
 }
 
+}  // namespace lms
+
+namespace lms {
+// ------------------------------------------------------------ codec (R15)
+// q[i] = binary16 bits of RNE(fp32(F * x[i])), saturated.
+__global__ void __launch_bounds__(256) k_compress(const float* __restrict__ x, int64_t n, float F,
+                                                  __half* __restrict__ q) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = enc1(__ldcs(x + i), F);
+}
+// x[i] = fp32(q[i]) / F.
+__global__ void __launch_bounds__(256) k_decompress(const __half* __restrict__ q, int64_t n,
+                                                    float F, float* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = dec1(q[i], F);
+}
+
+cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* out, int num_sms,
+                         cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  if (blocks < 1) blocks = 1;
+  if (down)
+    k_compress<<<(unsigned)blocks, 256, 0, s>>>((const float*)in, n, F, (__half*)out);
+  else
+    k_decompress<<<(unsigned)blocks, 256, 0, s>>>((const __half*)in, n, F, (float*)out);
+  return cudaGetLastError();
+}
 }  // namespace lms

@@ -82,6 +82,9 @@ _host_step = _sig("lmscale_train_step_host", _S,
                   [_P, _P, _P, _i64, _P, ctypes.c_float, _P, ctypes.POINTER(_i64), _P])
 _alloc_table = _sig("lmscale_alloc_table", _S, [_P, ctypes.POINTER(_P), ctypes.POINTER(_i64)])
 _set_timing = _sig("lmscale_set_timing", _S, [_P, ctypes.c_int])
+_set_compression = _sig("lmscale_set_compression", _S, [_P, ctypes.c_float])
+_compress = _sig("lmscale_compress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
+_decompress = _sig("lmscale_decompress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
 _get_stats = _sig("lmscale_get_stats", _S, [_P, ctypes.POINTER(StatsC)])
 _status_string = _sig("lmscale_status_string", ctypes.c_char_p, [_S])
 _last_error = _sig("lmscale_last_error", ctypes.c_char_p, [_P])
@@ -92,7 +95,7 @@ EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_u
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
             "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
             "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing", "lmscale_alloc_table",
-            "lmscale_get_stats",
+            "lmscale_set_compression", "lmscale_compress", "lmscale_decompress", "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
 
 
@@ -125,7 +128,8 @@ class _DevArray:
 
 
 def _view(ptr, shape, dtype, device):
-    typestr = {torch.uint32: "<u4", torch.int32: "<i4", torch.float32: "<f4"}[dtype]
+    typestr = {torch.uint32: "<u4", torch.int32: "<i4", torch.float32: "<f4",
+               torch.int16: "<i2"}[dtype]
     n = 1
     for s in shape:
         n *= s
@@ -312,6 +316,26 @@ class Context:
     def set_timing(self, mode: int):
         """0 none, 1 S4-only events, 2 every phase (see lmscale_set_timing)."""
         self._check(_set_timing(self._h, int(mode)), "lmscale_set_timing")
+
+    def set_compression(self, F: float):
+        """Sec. 3.3 compressed exchange for later collective steps; 0 = off."""
+        self._check(_set_compression(self._h, float(F)), "lmscale_set_compression")
+
+    def compress(self, x, F, stream=None) -> torch.Tensor:
+        """binary16 bits (as int16) of RNE(fp32(F * x)), saturated."""
+        assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+        q = torch.empty(x.shape, dtype=torch.int16, device=x.device)
+        self._check(_compress(self._h, _ptr(x), x.numel(), float(F), _ptr(q), _stream(stream)),
+                    "lmscale_compress")
+        return q
+
+    def decompress(self, q, F, stream=None) -> torch.Tensor:
+        """fp32(q) / F; q holds binary16 bits (int16 or float16 tensor)."""
+        assert q.is_cuda and q.element_size() == 2 and q.is_contiguous()
+        x = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        self._check(_decompress(self._h, _ptr(q), q.numel(), float(F), _ptr(x), _stream(stream)),
+                    "lmscale_decompress")
+        return x
 
     def stats(self) -> dict:
         s = StatsC()

@@ -21,7 +21,7 @@ import oracle  # noqa: E402
 import synth  # noqa: E402
 from paper_1810_10045_b200 import lmscale  # noqa: E402
 from paper_1810_10045_b200.distributed import make_context  # noqa: E402
-from tests.tolerances import check_rows  # noqa: E402
+from tests.tolerances import check_compressed_rows, check_rows, compressed_tol  # noqa: E402
 
 
 def u32(t):
@@ -124,15 +124,82 @@ def run_fused_small(cfg, mode, rank, G, dev, own_table=False):
     ctx.close()
 
 
-def run_full(cfg, rank, G, dev, n_rand=24, fused=False):
+def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
+    """lmscale_step with compression (Sec. 3.3, R15) against
+    oracle.sync_unique_compressed: INT mode bit-exact over the whole table,
+    float modes within compressed_tol; replicas bit-identical.  lr is taken
+    at fp32 precision on both sides so that equal M^ rows give equal E rows
+    (the GPU's fma rounds once, like the oracle's fp64 update)."""
+    lr = float(np.float32(synth.default_lr(mode)))
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    Dh = [synth.grad_values(cfg.K, cfg.D, mode, rank=g) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, mode)
+    ctx = make_context(cfg.V, cfg.K, cfg.D)
+    ctx.set_compression(F)
+    if own_table:
+        E = ctx.alloc_table()
+        E.copy_(E0.to(dev))
+        torch.cuda.synchronize()
+    else:
+        E = E0.to(dev)
+    ug = ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), E, lr,
+                  want_num_unique=True)
+    torch.cuda.synchronize()
+    assert ctx.stats()["fused_s5_s6"] == 3
+    Eo = E0.numpy().copy()
+    ref = oracle.sync_unique_compressed(J, [d.numpy() for d in Dh], Eo, lr, F)
+    assert ug == ref["Ug"]
+    got = E.cpu().numpy()
+    if mode == "int":
+        np.testing.assert_array_equal(got, Eo)
+    else:
+        t = ref["Ihat"].astype(np.int64)
+        A = oracle.abs_scale(J, [d.numpy() for d in Dh], ref["Ihat"])
+        E0n = E0.numpy()
+        tol = lr * compressed_tol(A, F, G) + 2.0 ** -23 * np.abs(E0n[t])
+        check_compressed_rows(got[t], Eo[t], tol, f"compressed G={G} {cfg.name} {mode} F={F}")
+        untouched = np.setdiff1d(np.arange(cfg.V), t)
+        np.testing.assert_array_equal(got[untouched], E0n[untouched])
+    check_replicas(E, f"compressed {cfg.name} {mode}")
+    ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), E, lr)
+    torch.cuda.synchronize()
+    check_replicas(E, f"compressed step 2 {cfg.name} {mode}")
+    # compression off again: the plain fused exchange on the same context
+    ctx.set_compression(0.0)
+    ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), Dh[rank].to(dev), E, lr)
+    torch.cuda.synchronize()
+    assert ctx.stats()["fused_s5_s6"] in (1, 2)
+    check_replicas(E, f"uncompressed after compressed {cfg.name} {mode}")
+    if rank == 0:
+        print(f"compressed G={G} {cfg.name} {mode} F={F} own_table={own_table}", flush=True)
+    ctx.close()
+
+
+def compressed_row(Js, Ds, w, F):
+    """Oracle M^ row of one word under compression, from the definition: each
+    rank's M_g row is the fp64 sum of its Delta rows of that word, rounded to
+    fp32 (absent: zeros), then the R15 codec around the fp32 rank-order sum."""
+    a = []
+    for Jg, Dg in zip(Js, Ds):
+        m, _, _ = oracle.type_gradient([Jg], [Dg], int(w))   # zeros when absent
+        a.append(oracle.decompress(oracle.compress(m.astype(np.float32), F), F))
+    s = oracle.sum_f32(a)
+    return oracle.decompress(oracle.compress(s, F), F)
+
+
+def run_full(cfg, rank, G, dev, n_rand=24, fused=False, F=0.0):
     """BASELINE full size on G real GPUs: integers in full, sampled float rows."""
     mode = "signed"
     lr = synth.default_lr(mode)
+    if F > 0:
+        lr = float(np.float32(lr))   # fp32 lr on both sides (see run_compressed_small)
     J = [synth.ids_for(cfg, g) for g in range(G)]
     ctx = make_context(cfg.V, cfg.K, cfg.D)
     grad = synth.grad_values(cfg.K, cfg.D, mode, rank=rank, device=dev)
     E = synth.table_values(cfg.V, cfg.D, mode, device=dev)
     Ihat, gcounts = oracle.unique_global(np.concatenate(J))
+    if F > 0:
+        ctx.set_compression(F)
     if fused:
         ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), grad, E, lr)
         torch.cuda.synchronize()
@@ -159,6 +226,13 @@ def run_full(cfg, rank, G, dev, n_rand=24, fused=False):
             Js.append(J[g][pos])
             Ds.append(synth.grad_rows(cfg.D, mode, pos, rank=g).numpy().reshape(len(pos), cfg.D))
         ref, A, n = oracle.type_gradient(Js, Ds, w)
+        if F > 0:
+            mh = compressed_row(Js, Ds, w, F).astype(np.float64)
+            tol = lr * compressed_tol(A, F, G) + 2.0 ** -23 * np.abs(E0[i])
+            expE = (E0[i] - lr * mh).astype(np.float32)       # one rounding (R5)
+            check_compressed_rows(gotE[i], expE, tol, f"{cfg.name} G={G} comp word {w}",
+                                  min_exact=0.9)
+            continue
         if got is not None:
             check_rows(got[i:i + 1], ref[None], A[None], mode, f"{cfg.name} G={G} word {w}")
         check_rows(gotE[i:i + 1], (E0[i] - lr * ref)[None], (np.abs(E0[i]) + lr * A)[None],
@@ -183,6 +257,15 @@ def main():
         run_fused_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
         for mode in ("int", "signed"):
             run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev, own_table=True)
+    if "comp" in which:
+        for F in (1.0, 1024.0):
+            run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "int", rank, G, dev, F)
+        run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "signed", rank, G, dev, 1.0)
+        run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "pos", rank, G, dev, 32.0,
+                             own_table=True)
+        run_compressed_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev,
+                             1.0)
+        run_full(synth.CONFIGS["1b"], rank, G, dev, fused=True, F=1.0)
     for name in ("1b", "char", "amazon", "tieba"):
         if name in which:
             run_full(synth.CONFIGS[name], rank, G, dev)

@@ -394,3 +394,50 @@ def test_full_size_emulated_ranks_integers_and_sampled_rows(lm, name, G):
         assert n == gcounts[slots[i]]
         check_rows(got[i:i + 1], ref[None], A[None], mode, f"{name} G={G} word {w}")
     ctx.close()
+
+
+# ------------------------------------------------------------ compression
+
+@pytest.mark.parametrize("F", [1.0, 3.0, 256.0, 1024.0])
+def test_codec_bit_exact(lm, F):
+    """lmscale_compress / lmscale_decompress (R15) against the
+    oracle codec, element by element, including subnormals, ties and
+    saturation; decompress over every finite binary16 bit pattern."""
+    rng = np.random.default_rng(int(F))
+    x = np.concatenate([
+        rng.standard_normal(100_003).astype(np.float32),
+        (rng.standard_normal(50_000) * 1e-6).astype(np.float32),
+        (rng.standard_normal(20_000) * 1e5).astype(np.float32),
+        rng.integers(-4096, 4096, 20_000).astype(np.float32) + 0.5,
+        np.float32([0.0, -0.0, 2.0 ** -25, -(2.0 ** -25), 65504.0, 65520.0, 1e30, -1e30]),
+    ])
+    ctx = lm.Context(16, 16, 4)
+    q = ctx.compress(torch.from_numpy(x).to(dev()), F)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(q.cpu().numpy().view(np.uint16), oracle.compress(x, F))
+    bits = np.arange(1 << 16, dtype=np.uint16)
+    bits = bits[np.isfinite(bits.view(np.float16))]
+    back = ctx.decompress(torch.from_numpy(bits.view(np.int16)).to(dev()), F)
+    np.testing.assert_array_equal(back.cpu().numpy(), oracle.decompress(bits, F))
+    assert ctx.compress(torch.empty(0, device=dev()), F).numel() == 0
+    with pytest.raises(lm.LmscaleError):
+        ctx.compress(torch.ones(4, device=dev()), 0.0)
+    ctx.close()
+
+
+def test_compression_is_noop_at_world1(lm):
+    """World 1 has no communication (R15): compression on or off, the step is
+    the same bits."""
+    cfg = synth.CONFIGS["tiny"]
+    J = to_dev_ids(synth.ids_for(cfg, 0))
+    g = synth.grad_values(cfg.K, cfg.D, "signed", rank=0, device=dev())
+    outs = []
+    for F in (0.0, 1024.0):
+        ctx = lm.Context(cfg.V, cfg.K, cfg.D)
+        ctx.set_compression(F)
+        E = synth.table_values(cfg.V, cfg.D, "signed", device=dev())
+        ctx.step(J, g, E, 0.1)
+        torch.cuda.synchronize()
+        outs.append(E.cpu())
+        ctx.close()
+    assert torch.equal(outs[0], outs[1])

@@ -71,3 +71,13 @@ def test_nccl_exchange_matches_oracle(n):
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     _torchrun(n, ["small", "1b", "char"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 4])
+def test_compressed_exchange_matches_oracle(n):
+    """Sec. 3.3 compression on real GPUs (R15): INT bit-exact, float modes
+    within the compressed tolerance, 1b full size on sampled rows."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    _torchrun(n, ["comp"])

@@ -33,3 +33,26 @@ def check_rows(got, ref64, absscale64, mode, what=""):
     worst = float(rel.max()) if rel.size else 0.0
     assert worst <= RTOL, f"{what}: max scaled error {worst:.3e} > {RTOL}"
     return worst
+
+
+def compressed_tol(absscale64, F, G):
+    """Bound on |GPU - oracle| for a row of M^ from the compressed exchange
+    (R15 / "Tolerances"): each side is within
+    2^-10 (sum_g |M_g| + |M^|) + (G + 1) 2^-24 / F of the exact sum (one
+    binary16 rounding per transfer, pinned in tests/test_compression_oracle.py),
+    and sum_g |M_g|, |M^| <= A, so the two sides differ by at most
+    2^-8 A + (G + 1) 2^-23 / F."""
+    return 2.0 ** -8 * np.asarray(absscale64, np.float64) + (G + 1) * 2.0 ** -23 / F
+
+
+def check_compressed_rows(got, ref, tol, what="", min_exact=0.99):
+    """|got - ref| <= tol everywhere, and at least `min_exact` of the elements
+    bit-identical (the two sides differ only where an fp32 summation-order
+    difference crosses a binary16 rounding boundary)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(got - ref)
+    assert (err <= tol).all(), f"{what}: max err {err.max():.3e}, tol at worst {tol.ravel()[np.argmax(err - tol)]:.3e}"
+    if got.size:
+        frac = float((got == ref).mean())
+        assert frac >= min_exact, f"{what}: only {frac:.4f} of elements bit-identical"
