@@ -373,8 +373,15 @@ def main():
     hbm_peak, peak_kind = peaks()
     st_last = ctx.stats()
     D = cfg.D
-    kname = "k_scatter (S4 segmented scatter-add + cut-run fixup, one cooperative launch)"
-    scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
+    inline_s6 = world == 1 and not os.environ.get("LMSCALE_NO_INLINE_S6")
+    if inline_s6:
+        # world 1: S6 folded into S4 -- grad read once, each E row of I^ read
+        # and written once; M is never materialised
+        kname = "k_scatter (S4 segmented scatter-add + folded S6 row update, one launch)"
+        scatter_bytes = 4 * cfg.K * D + 8 * ug * D
+    else:
+        kname = "k_scatter (S4 segmented scatter-add + cut-run fixup, one launch)"
+        scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
     scatter_us = s4_us
     roof = {"kernel": kname, "bound": "hbm",
             "achieved": scatter_bytes / (scatter_us * 1e-6) / 1e9, "peak": hbm_peak,
@@ -414,6 +421,9 @@ def main():
                "achieved": nvl / (ph["us_allreduce"] * 1e-6) / 1e9, "peak": 770.0,
                "peak_kind": "guide: measured peer copy per direction (900 nominal)"}
         upd["frac"] = upd["achieved"] / upd["peak"]
+    elif inline_s6:
+        upd = {"kernel": "folded into k_scatter (world 1)", "achieved": None,
+               "bytes_per_launch": 0, "us_per_launch": 0.0, "frac": None}
     else:
         update_bytes = 12 * ug * D
         upd = {"kernel": "k_update (S6 row update)", "achieved": update_bytes /

@@ -126,6 +126,7 @@ struct ScatterArgs {
   int zero_rows;          // 0: every slot is present locally (world 1): slot = local index
   int fill_absent;        // zero the M rows of slots absent on this rank (world > 1)
   int m16;                // M rows are stored compressed (binary16 of cF * x, R15)
+  int apply;              // world 1: S6 folded in -- finished rows update `table`, no M
   float cF;               // compression scale F
   int short_runs;         // finish runs <= FX_SHORT in their starting chunk (large K)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
@@ -149,7 +150,7 @@ cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* ou
 // n_dev != nullptr: the row count is read on the device (min(n, *n_dev)); n
 // is then the capacity that sizes the grid.
 void launch_update(float* table, int D, const uint32_t* ids, const float* rows, int64_t n,
-                   const int64_t* n_dev, float lr, int num_sms, cudaStream_t s);
+                   const Sc3* n_dev, float lr, int num_sms, cudaStream_t s);
 void launch_dense(float* table, int D, const uint32_t* ids, const float* grad, int64_t n,
                   float lr, uint32_t vocab, int num_sms, cudaStream_t s);
 

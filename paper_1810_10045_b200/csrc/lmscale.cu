@@ -305,6 +305,7 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fill_absent = 1;
   a.m16 = 0;
   a.cF = 0.f;
+  a.apply = 0;
   a.short_runs = ctx->last_k >= (1 << 16) ? 1 : 0;
   a.table = nullptr;
   a.lr = 0.f;
@@ -320,10 +321,11 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
 // S4 (+ the world-1 S6 when table != nullptr): one cooperative launch.
 lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
                       float* table = nullptr, float lr = 0.f, bool fill_absent = true,
-                      float m16_F = 0.f) {
+                      float m16_F = 0.f, bool apply = false) {
   ScatterArgs a = scatter_args(ctx, grad);
   a.table = table;
   a.lr = lr;
+  a.apply = apply ? 1 : 0;
   a.fill_absent = fill_absent ? 1 : 0;
   a.m16 = m16_F > 0.f ? 1 : 0;
   a.cF = m16_F;
@@ -809,8 +811,12 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   const bool comp = G > 1 && ctx->cF > 0.f;
   const bool p2p = G > 1 && table && ctx->nvls &&
                    (comp || (table == ctx->table_ptr && ctx->table_win && nvls_use_p2p(G)));
-  st = run_s4(ctx, grad, s, fuse_s6 ? table : nullptr, lr, /*fill_absent=*/G > 1 && !p2p,
-              comp ? ctx->cF : 0.f);
+  // world 1: S6 folded into S4 (finished rows go straight into the table; M
+  // is not written and not re-read).  LMSCALE_NO_INLINE_S6: separate k_update.
+  static const bool no_inline = getenv("LMSCALE_NO_INLINE_S6") != nullptr;
+  const bool inline_s6 = G == 1 && table && !no_inline;
+  st = run_s4(ctx, grad, s, (fuse_s6 || inline_s6) ? table : nullptr, lr,
+              /*fill_absent=*/G > 1 && !p2p, comp ? ctx->cF : 0.f, inline_s6);
   if (st) return st;
   rec(ctx, EV_FIXUP_END, s);
   if (G > 1 && table && ctx->nvls) {
@@ -861,9 +867,10 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     // S6 straight away with the device-side count: no host round trip.
     rec(ctx, EV_AR_END, s);
     rec(ctx, EV_UPD_BEGIN, s);
-    launch_update(table, (int)D, ctx->ihat, ctx->M, ctx->ucap, &ctx->sc3->u_global, lr,
-                  ctx->num_sms, s);
-    LAUNCHED(1);
+    if (!inline_s6) {
+      launch_update(table, (int)D, ctx->ihat, ctx->M, ctx->ucap, ctx->sc3, lr, ctx->num_sms, s);
+      LAUNCHED(1);
+    }
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
@@ -871,7 +878,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     print_trace(ctx, s);
     if (out) {
       out->ids = ctx->ihat;
-      out->rows = ctx->M;
+      out->rows = inline_s6 ? nullptr : ctx->M;  // folded S6 consumed the rows
       out->num_unique = -1;
     }
     end_call(ctx);
@@ -895,7 +902,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   rec(ctx, EV_AR_END, s);
   if (table) {
     rec(ctx, EV_UPD_BEGIN, s);
-    if (!fuse_s6) {
+    if (!fuse_s6 && !inline_s6) {
       launch_update(table, (int)D, ctx->ihat, ctx->M, ug, nullptr, lr, ctx->num_sms, s);
       if (ug > 0) LAUNCHED(1);
     }
@@ -906,7 +913,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
 
   if (out) {
     out->ids = ctx->ihat;
-    out->rows = ctx->M;
+    out->rows = inline_s6 ? nullptr : ctx->M;
     out->num_unique = ug;
   }
   ctx->stats.bytes_ids_gathered = 4 * (int64_t)(G - 1) * k;

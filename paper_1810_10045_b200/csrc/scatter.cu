@@ -71,6 +71,46 @@ __device__ __forceinline__ void st_m(const ScatterArgs& a, size_t slot, int C, i
     a.M[slot * C + col] = v;
 }
 
+
+// World 1 with S6 folded in (a.apply): a finished row m of word w goes straight
+// into the table, E[w] = fma(-lr, m, E[w]) -- the same instruction k_update
+// runs, so the bits equal the separate-launch path; M is never written.
+template <typename T>
+__device__ __forceinline__ void apply_e(const ScatterArgs& a, uint32_t w, int C, int col, T m);
+template <>
+__device__ __forceinline__ void apply_e<float4>(const ScatterArgs& a, uint32_t w, int C, int col,
+                                                float4 m) {
+  float4* e = reinterpret_cast<float4*>(a.table) + (size_t)w * C + col;
+  const float4 x = *e;
+  st_v4(e, make_float4(__fmaf_rn(-a.lr, m.x, x.x), __fmaf_rn(-a.lr, m.y, x.y),
+                       __fmaf_rn(-a.lr, m.z, x.z), __fmaf_rn(-a.lr, m.w, x.w)));
+}
+template <>
+__device__ __forceinline__ void apply_e<float>(const ScatterArgs& a, uint32_t w, int C, int col,
+                                               float m) {
+  float* e = a.table + (size_t)w * C + col;
+  *e = __fmaf_rn(-a.lr, m, *e);
+}
+
+// A finished row of slot `slot` (word w): into M, or into E (a.apply).
+template <typename T, int NV, bool FULLC>
+__device__ __forceinline__ void emit_row(const ScatterArgs& a, size_t slot, uint32_t w, int C,
+                                         int col0, const T (&acc)[NV]) {
+  if (a.apply) {
+    T* e = reinterpret_cast<T*>(a.table) + (size_t)w * C;
+    T x[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (FULLC || col0 + v * 32 < C) x[v] = e[col0 + v * 32];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (FULLC || col0 + v * 32 < C) Vec<T>::st(e + col0 + v * 32, Vec<T>::fma(-a.lr, acc[v], x[v]));
+  } else {
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (FULLC || col0 + v * 32 < C) st_m(a, slot, C, col0 + v * 32, acc[v]);
+  }
+}
 }  // namespace
 
 // ------------------------------------------------------------------- S4
@@ -82,7 +122,7 @@ __device__ __forceinline__ void st_m(const ScatterArgs& a, size_t slot, int C, i
 // Only long runs (the Zipf head) are cut into partial rows (P[2c] head piece,
 // P[2c+1] tail piece) and listed for the fix-up phase by the chunk holding
 // their start.  FULLC: the column block lies inside the row (no predicates).
-template <typename T, int NV, int UNR, bool FULLC>
+template <typename T, int NV, int UNR, bool FULLC, bool PRE>
 __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __restrict__ g,
                                               T* __restrict__ M, T* __restrict__ P, int c,
                                               int n, int col0, int C, int lane) {
@@ -110,6 +150,8 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
   // world 1: I^ = J^, so the slot is the run index itself (no dependent load)
   int my_slot = -1;
   if (lane < n) my_slot = a.zero_rows ? __ldg(a.l2g + my_u) : my_u;
+  uint32_t my_w = 0;  // the run's word (world-1 S6 folded in)
+  if (a.apply && lane < n) my_w = __ldg(a.ihat + my_slot);
   const int f_start = __shfl_sync(FULL_MASK, ls, 0), f_end = __shfl_sync(FULL_MASK, ls, 1);
   const int l_start = __shfl_sync(FULL_MASK, ls, 2), l_end = __shfl_sync(FULL_MASK, ls, 3);
   // without short-run handling (small K, where the fix-up is cheap) every cut
@@ -141,6 +183,25 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
         const int col = col0 + v * 32;
         r[q][v] = V::zero();
         if (p < p_end && (FULLC || col < C)) r[q][v] = V::ld_once(row + col);
+      }
+    }
+    // PRE (world-1 folded S6, small K): the E rows of the runs ending in this
+    // group are loaded together with the gradient rows, so the row update at
+    // a run's end does not wait for a dependent load (p_end <= n here)
+    T x[PRE ? UNR : 1][NV];
+    if constexpr (PRE) {
+      const T* E = reinterpret_cast<const T*>(a.table);
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int p = p0 + q;
+        const bool endp = p < p_end && (p == p_end - 1 || (p + 1 < n && ((hmask >> (p + 1)) & 1u)));
+        const uint32_t wq = __shfl_sync(FULL_MASK, my_w, min(p, n - 1));
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int col = col0 + v * 32;
+          x[q][v] = V::zero();
+          if (endp && (FULLC || col < C)) x[q][v] = E[(size_t)wq * C + col];
+        }
       }
     }
 #pragma unroll
@@ -175,12 +236,15 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
             }
           } else {
             dst = nullptr;
-            if (slot >= 0) {
+            const uint32_t wv = __shfl_sync(FULL_MASK, my_w, min(p, n - 1));
+            if constexpr (PRE) {
+              T* e = reinterpret_cast<T*>(a.table) + (size_t)wv * C;
 #pragma unroll
-              for (int v = 0; v < NV; ++v) {
-                const int col = col0 + v * 32;
-                if (FULLC || col < C) st_m(a, (size_t)slot, C, col, acc[v]);
-              }
+              for (int v = 0; v < NV; ++v)
+                if (FULLC || col0 + v * 32 < C)
+                  V::st(e + col0 + v * 32, V::fma(-a.lr, acc[v], x[q][v]));
+            } else if (slot >= 0) {
+              emit_row<T, NV, FULLC>(a, (size_t)slot, wv, C, col0, acc);
             }
           }
           if (dst) {
@@ -246,6 +310,7 @@ __device__ __forceinline__ void fixup_part(const ScatterArgs& a, T (*red)[32 * N
   __syncthreads();
   if (warp == 0) {
     const int slot = nparts == 1 ? (a.zero_rows ? __ldcg(a.l2g + u) : u) : -1;
+    const uint32_t word = (a.apply && slot >= 0) ? __ldg(a.ihat + slot) : 0u;
     T* dst = nparts == 1 ? nullptr : reinterpret_cast<T*>(a.part2) + (size_t)e * C;
     if (dst || slot >= 0) {
 #pragma unroll
@@ -257,6 +322,8 @@ __device__ __forceinline__ void fixup_part(const ScatterArgs& a, T (*red)[32 * N
         if (col < C) {
           if (dst)
             V::st(dst + col, sum);
+          else if (a.apply)
+            apply_e<T>(a, word, C, col, sum);
           else
             st_m(a, (size_t)slot, C, col, sum);
         }
@@ -280,13 +347,17 @@ __device__ __forceinline__ void fixup_final(const ScatterArgs& a, int e0, int cb
   if (slot < 0) return;
   const T* L2 = reinterpret_cast<const T*>(a.part2);
   const int col0 = cb * 32 * NV + lane;
+  const uint32_t w = a.apply ? __ldg(a.ihat + slot) : 0u;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const int col = col0 + v * 32;
     if (col >= C) continue;
     T sum = V::ld_l2(L2 + (size_t)e0 * C + col);
     for (int j = 1; j < nparts; ++j) sum = V::add(sum, V::ld_l2(L2 + (size_t)(e0 + j) * C + col));
-    st_m(a, (size_t)slot, C, col, sum);
+    if (a.apply)
+      apply_e<T>(a, w, C, col, sum);
+    else
+      st_m(a, (size_t)slot, C, col, sum);
   }
 }
 
@@ -299,8 +370,8 @@ __device__ __forceinline__ void sstamp(unsigned long long* tr, int i) {
   }
 }
 
-template <typename T, int NV, int UNR>
-__global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
+template <typename T, int NV, int UNR, bool PRE>
+__global__ void __launch_bounds__(SC_THREADS, PRE ? 1 : 2) k_scatter(ScatterArgs a) {
   using V = Vec<T>;
   sstamp(a.trace, 54);
   if (a.trace && threadIdx.x == 0) {  // earliest start over all CTAs (as ~t)
@@ -309,6 +380,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
     atomicMax(a.trace + 63, ~t);
   }
   __shared__ T red[SC_THREADS / 32][32 * NV];
+  // an id >= vocab: no table row is touched (the error surfaces at the next
+  // host sync); every CTA reads the same flag, so all leave together
+  if (a.apply && (__ldcg(&a.sc3->err) & 1u)) return;
   const int K = a.K;
   const int C = a.D / V::W;  // vectors per row
   const int ncb = (C + 32 * NV - 1) / (32 * NV);
@@ -331,9 +405,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
       const int c = (int)unit;
       const int n = min(SC_CHUNK, K - c * SC_CHUNK);
       if ((cb + 1) * 32 * NV <= C)
-        scatter_chunk<T, NV, UNR, true>(a, g, M, P, c, n, col0, C, lane);
+        scatter_chunk<T, NV, UNR, true, PRE>(a, g, M, P, c, n, col0, C, lane);
       else
-        scatter_chunk<T, NV, UNR, false>(a, g, M, P, c, n, col0, C, lane);
+        scatter_chunk<T, NV, UNR, false, PRE>(a, g, M, P, c, n, col0, C, lane);
     } else {
       // ---- zero rows: slots [r0, r0 + 32) whose word is absent on this rank
       const int64_t r0 = (unit - nchunks) * SC_ZGROUP;
@@ -375,7 +449,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scatter(ScatterArgs a) {
     if ((en.y & 0xffff) == 0 && (en.y >> 16) > 1) fixup_final<T, NV>(a, e, (int)(it % ncb), C);
   }
 
-  if (!a.table) return;
+  if (!a.table || a.apply) return;
   grid_barrier(a.bar);
 
   // phase 3 (world 1): S6 row update, warp per row
@@ -408,12 +482,12 @@ bool vec_ok(const ScatterArgs& a) {
 }
 }  // namespace
 
-template <typename T, int NV, int UNR>
+template <typename T, int NV, int UNR, bool PRE = false>
 static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   static int occ = 0;  // resident CTAs per SM for this instantiation (persistent grid)
   if (!occ) {
-    max_carveout((const void*)k_scatter<T, NV, UNR>);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<T, NV, UNR>, SC_THREADS,
+    max_carveout((const void*)k_scatter<T, NV, UNR, PRE>);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<T, NV, UNR, PRE>, SC_THREADS,
                                                       0) != cudaSuccess || occ < 1)
       occ = 1;
   }
@@ -427,13 +501,25 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phases 2/3 want a wide grid
   // grid <= occupancy x SMs: every CTA is co-resident, so the in-kernel
   // grid barrier is safe with a normal launch
-  k_scatter<T, NV, UNR><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
+  k_scatter<T, NV, UNR, PRE><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
   if (vec_ok<float4>(a)) {
     const int C = a.D / 4;
+    // experiment knob: column-block width x row loads in flight per warp
+    static const int var = getenv("LMSCALE_S4_VARIANT") ? atoi(getenv("LMSCALE_S4_VARIANT")) : 0;
+    // folded S6 at small K (no short-run extension): E rows preloaded per group
+    static const bool no_pre = getenv("LMSCALE_NO_PRE") != nullptr;
+    if (a.apply && !a.short_runs && !no_pre) {
+      if (C >= 128) return scatter_t<float4, 4, 4, true>(a, s);
+      if (C >= 64) return scatter_t<float4, 2, 4, true>(a, s);
+      return scatter_t<float4, 1, 4, true>(a, s);
+    }
+    if (var == 1) return scatter_t<float4, 2, 8>(a, s);
+    if (var == 2) return scatter_t<float4, 1, 16>(a, s);
+    if (var == 3) return scatter_t<float4, 1, 8>(a, s);
     if (C >= 128) return scatter_t<float4, 4, 4>(a, s);
     if (C >= 64) return scatter_t<float4, 2, 4>(a, s);
     return scatter_t<float4, 1, 4>(a, s);
@@ -448,9 +534,12 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_update(float* __restrict__ table, int D,
                                                 const uint32_t* __restrict__ ids,
                                                 const float* __restrict__ rows, int64_t n,
-                                                const int64_t* __restrict__ n_dev, float lr) {
+                                                const Sc3* __restrict__ n_dev, float lr) {
   using V = Vec<T>;
-  if (n_dev) n = min(n, *n_dev);  // device-side count (no host round trip)
+  if (n_dev) {  // device-side count (no host round trip); nothing on an id error
+    if (n_dev->err & 1u) return;
+    n = min(n, n_dev->u_global);
+  }
   const int C = D / V::W;
   const int lane = (int)lane_id();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -475,7 +564,7 @@ __global__ void __launch_bounds__(256) k_update(float* __restrict__ table, int D
 }
 
 void launch_update(float* table, int D, const uint32_t* ids, const float* rows, int64_t n,
-                   const int64_t* n_dev, float lr, int num_sms, cudaStream_t s) {
+                   const Sc3* n_dev, float lr, int num_sms, cudaStream_t s) {
   if (n <= 0) return;
   int64_t blocks = (n + 7) / 8;
   const int64_t cap = (int64_t)num_sms * 8;

@@ -441,3 +441,21 @@ def test_compression_is_noop_at_world1(lm):
         outs.append(E.cpu())
         ctx.close()
     assert torch.equal(outs[0], outs[1])
+
+
+def test_step_with_bad_id_leaves_table_untouched(lm):
+    """World-1 step without a host sync (S6 folded into S4): an id >= vocab
+    must not touch any table row; the error surfaces at the next host sync."""
+    ctx = lm.Context(100, 64, 8)
+    E = torch.ones(100, 8, device=dev())
+    ids = to_dev_ids(np.array([1, 2, 100, 3], np.uint32))
+    ctx.step(ids, torch.ones(4, 8, device=dev()), E, 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(E, torch.ones(100, 8, device=dev()))
+    with pytest.raises(lm.LmscaleError) as e:
+        ctx.sparse_grad()
+    assert e.value.status == lm.ID_RANGE
+    ctx.step(to_dev_ids(np.array([1, 2, 2, 3], np.uint32)), torch.ones(4, 8, device=dev()), E, 0.5)
+    torch.cuda.synchronize()
+    assert E[2, 0].item() == 0.0 and E[1, 0].item() == 0.5 and E[0, 0].item() == 1.0
+    ctx.close()
