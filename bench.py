@@ -379,6 +379,13 @@ def main():
         # and written once; M is never materialised
         kname = "k_scatter (S4 segmented scatter-add + folded S6 row update, one launch)"
         scatter_bytes = 4 * cfg.K * D + 8 * ug * D
+    elif st_last.get("fused_s5_s6") in (2, 3):
+        # fused P2P exchange: only the present rows of M_g are written
+        # (fp32, or binary16 with compression)
+        esz = 2 if st_last.get("fused_s5_s6") == 3 else 4
+        kname = ("k_scatter (S4 segmented scatter-add, present rows only"
+                 + (", binary16 output)" if esz == 2 else ")"))
+        scatter_bytes = 4 * cfg.K * D + esz * int(info.get("u_local") or 0) * D
     else:
         kname = "k_scatter (S4 segmented scatter-add + cut-run fixup, one launch)"
         scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
