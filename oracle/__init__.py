@@ -80,6 +80,14 @@ def _load():
             lib.oracle_decompress.argtypes = [P, i64, ctypes.c_float, P]
             lib.oracle_sum_f32.restype = None
             lib.oracle_sum_f32.argtypes = [P, ctypes.c_int, i64, P]
+            lib.oracle_mix64.restype = ctypes.c_uint64
+            lib.oracle_mix64.argtypes = [ctypes.c_uint64]
+            lib.oracle_draw_one.restype = ctypes.c_uint32
+            lib.oracle_draw_one.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.c_uint64]
+            lib.oracle_draw_samples.restype = i64
+            lib.oracle_draw_samples.argtypes = [ctypes.c_uint64, ctypes.c_uint64, i64,
+                                                ctypes.c_uint64, P]
             lib.oracle_type_gradient.argtypes = [P, P, P, ctypes.c_int, i64,
                                                  ctypes.c_uint32, P, P]
             _lib = lib
@@ -282,6 +290,57 @@ def sync_unique_compressed(J_list, delta_list, E, lr, F):
     update_rows(E, Ihat, Mhat.astype(np.float64), lr)    # step 7
     return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M32=M32, Q=Q, S=S,
                 Qhat=Qhat, Mhat=Mhat, E=E)
+
+
+# ------------------------------------------------------------ seeding (3.2)
+
+SEED_POLICIES = ("distinct", "same", "log2", "loge", "log10", "power")
+
+
+def plan_seeds(G, policy, alpha=0.64, master_seed=0):
+    """Seed groups of Sec. 3.2 (R16): "make a subset of GPUs use the
+    same seed"; policies all-distinct, all-same, log2/ln/log10 of G ("number of
+    seeds equal to log2, loge, and log10 of the number of GPUs") and
+    G^alpha ("we only need G^alpha unique random seeds").  Group counts
+    as SPEC S:325: log_b -> max(1, round(log_b G)), power -> max(1, ceil(G^a)).
+    Ranks go to groups in contiguous blocks: group(r) = floor(r * n / G).
+    Seed of group q = mix64(master_seed + q).  Returns (seeds[G], n_groups)."""
+    import math
+    if policy == "distinct":
+        n = G
+    elif policy == "same":
+        n = 1
+    elif policy in ("log2", "loge", "log10"):
+        b = {"log2": 2.0, "loge": math.e, "log10": 10.0}[policy]
+        n = max(1, int(math.floor(math.log(G) / math.log(b) + 0.5)))
+    elif policy == "power":
+        if not (0.0 < alpha <= 1.0):
+            raise ValueError("alpha must be in (0, 1]")
+        n = max(1, int(math.ceil(G ** alpha)))
+    else:
+        raise ValueError(policy)
+    n = min(n, G)
+    lib = _load()
+    seeds = [int(lib.oracle_mix64((master_seed + (r * n) // G) & (2**64 - 1))) for r in range(G)]
+    return seeds, n
+
+
+def draw_samples(seed, step, S, V):
+    """The first S distinct values of the R16 stream, in stream order (uint32)."""
+    if S > V:
+        raise ValueError("S > V")
+    lib = _load()
+    out = np.empty(S, np.uint32)
+    lib.oracle_draw_samples(seed & (2**64 - 1), step & (2**64 - 1), S, V, _p(out))
+    return out
+
+
+def draw_one(seed, step, i, V):
+    return int(_load().oracle_draw_one(seed, step, i, V))
+
+
+def mix64(z):
+    return int(_load().oracle_mix64(z & (2**64 - 1)))
 
 
 def sync_dense(J_list, delta_list, E, lr):

@@ -258,3 +258,41 @@ void oracle_sum_f32(const float* const* a, int G, int64_t n, float* out) {
   for (int g = 0; g < G; ++g)
     for (int64_t i = 0; i < n; ++i) out[i] += a[g][i];
 }
+
+/*
+ * Seeding (Sec. 3.2; reading R16).  The sampled-softmax
+ * candidates of a GPU are S words drawn "randomly" (P:263-264, 1024 per GPU at
+ * P:605); GPUs of one seed group share the seed and so draw the same words.
+ * R16 fixes the draw: uniform without replacement = the first S distinct
+ * values of the stream x_i = floor(u_i * V / 2^64), i = 0, 1, 2, ..., with
+ * u_i = mix64(A + i) and A = mix64(seed ^ mix64(step)), where mix64 is the
+ * SplitMix64 output function (state + golden gamma, two xor-shift-multiplies).
+ */
+uint64_t oracle_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* x_i of the stream above (one draw). */
+uint32_t oracle_draw_one(uint64_t seed, uint64_t step, uint64_t i, uint64_t V) {
+  uint64_t A = oracle_mix64(seed ^ oracle_mix64(step));
+  uint64_t u = oracle_mix64(A + i);
+  return (uint32_t)(((unsigned __int128)u * V) >> 64);
+}
+
+/* The first S distinct values of the stream, in stream order (plain linear
+ * membership test).  Requires S <= V.  Returns the number of draws used. */
+int64_t oracle_draw_samples(uint64_t seed, uint64_t step, int64_t S, uint64_t V, uint32_t* out) {
+  int64_t n = 0, i = 0;
+  while (n < S) {
+    uint32_t x = oracle_draw_one(seed, step, (uint64_t)i, V);
+    ++i;
+    int seen = 0;
+    for (int64_t j = 0; j < n; ++j)
+      if (out[j] == x) { seen = 1; break; }
+    if (!seen) out[n++] = x;
+  }
+  return i;
+}
