@@ -43,6 +43,12 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches (no CUDA graph)")
+    ap.add_argument("--seeding", default=None,
+                    choices=["distinct", "same", "log2", "loge", "log10", "power"],
+                    help="Sec. 3.2 output-embedding exchange: each step draws --samples "
+                         "candidates per GPU with its seed group's seed, then exchanges "
+                         "[K targets || samples]")
+    ap.add_argument("--samples", type=int, default=1024, help="sampled-softmax S per GPU (P:605)")
     ap.add_argument("--compress", type=float, default=0.0,
                     help="Sec. 3.3 compressed exchange with scale F (0 = off, fp32 rows)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -181,7 +187,10 @@ def config_dict(cfg, args, world):
             "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read sweep), "
                   "outside the timed region",
             "cuda_graph": not getattr(args, "no_graph", True),
-            "compression": f"fp16:F={args.compress:g}" if args.compress > 0 else "off"}
+            "compression": f"fp16:F={args.compress:g}" if args.compress > 0 else "off",
+            "seeding": (f"{args.seeding} (alpha 0.64), S={args.samples} samples/GPU; ids per "
+                        f"GPU = K targets + S samples" if getattr(args, "seeding", None)
+                        else "off (input-embedding exchange)")}
 
 
 def emit(line, args):
@@ -223,8 +232,11 @@ def main():
 
     # ---- inputs resident in HBM (seeded, per rank)
     J = synth.ids_for(cfg, rank)
-    ids = torch.from_numpy(J.view(np.int32)).to(dev)
-    grad = synth.grad_values(cfg.K, cfg.D, args.mode, rank=rank, device=dev)
+    S_smp = args.samples if args.seeding else 0
+    Kt = cfg.K + S_smp            # ids per GPU in the exchange
+    ids = torch.empty(Kt, dtype=torch.int32, device=dev)
+    ids[:cfg.K] = torch.from_numpy(J.view(np.int32)).to(dev)
+    grad = synth.grad_values(Kt, cfg.D, args.mode, rank=rank, device=dev)
     lr = synth.default_lr(args.mode)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     sweep = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -241,9 +253,14 @@ def main():
 
     flags = 0 if args.no_graph else lmscale.FLAG_GRAPH
     if world > 1:
-        ctx = make_context(cfg.V, cfg.K, cfg.D, flags=flags)
+        ctx = make_context(cfg.V, Kt, cfg.D, flags=flags)
     else:
-        ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, device=local, flags=flags)
+        ctx = lmscale.Context(cfg.V, Kt, cfg.D, device=local, flags=flags)
+    seed_plan = None
+    if args.seeding:
+        seeds, ngroups = lmscale.plan_seeds(world, args.seeding, 0.64, master_seed=synth.MASTER_SEED)
+        seed_plan = {"policy": args.seeding, "groups": ngroups, "samples_per_gpu": S_smp}
+        ctx.draw_samples(seeds[rank], 0, S_smp, out=ids[cfg.K:])
     # the table: with G > 1 the context allocates it in a symmetric window so
     # the fused S5+S6 kernel multicasts updated rows into every replica
     if world > 1:
@@ -291,7 +308,12 @@ def main():
     info = {}
     launches = [0]
 
+    step_no = [0]
+
     def step():
+        if seed_plan:   # this step's candidates (same words within a seed group)
+            step_no[0] += 1
+            ctx.draw_samples(seeds[rank], step_no[0], S_smp, out=ids[cfg.K:])
         ctx.step(ids, grad, table, lr)
 
     def collect():
@@ -378,17 +400,17 @@ def main():
         # world 1: S6 folded into S4 -- grad read once, each E row of I^ read
         # and written once; M is never materialised
         kname = "k_scatter (S4 segmented scatter-add + folded S6 row update, one launch)"
-        scatter_bytes = 4 * cfg.K * D + 8 * ug * D
+        scatter_bytes = 4 * Kt * D + 8 * ug * D
     elif st_last.get("fused_s5_s6") in (2, 3):
         # fused P2P exchange: only the present rows of M_g are written
         # (fp32, or binary16 with compression)
         esz = 2 if st_last.get("fused_s5_s6") == 3 else 4
         kname = ("k_scatter (S4 segmented scatter-add, present rows only"
                  + (", binary16 output)" if esz == 2 else ")"))
-        scatter_bytes = 4 * cfg.K * D + esz * int(info.get("u_local") or 0) * D
+        scatter_bytes = 4 * Kt * D + esz * int(info.get("u_local") or 0) * D
     else:
         kname = "k_scatter (S4 segmented scatter-add + cut-run fixup, one launch)"
-        scatter_bytes = 4 * cfg.K * D + 4 * ug * D   # grad read + M written once
+        scatter_bytes = 4 * Kt * D + 4 * ug * D   # grad read + M written once
     scatter_us = s4_us
     roof = {"kernel": kname, "bound": "hbm",
             "achieved": scatter_bytes / (scatter_us * 1e-6) / 1e9, "peak": hbm_peak,
@@ -447,7 +469,7 @@ def main():
                         min(args.warmup, 3))
             dense_ms = max_over_ranks(sum(dms), dev) / args.steps
             del table_d
-            ratio_model = (world * cfg.K * cfg.D) / (world * cfg.K + ug * cfg.D)
+            ratio_model = (world * Kt * cfg.D) / (world * Kt + ug * cfg.D)
             dense = {"ms_per_step": dense_ms, "tokens_per_s": tokens / (dense_ms * 1e-3),
                      "speedup_unique_vs_dense": dense_ms / ms_step,
                      "paper_ratio_GKD_over_GK_plus_UD": ratio_model,
@@ -457,7 +479,9 @@ def main():
 
     # ---- e2e: host (pinned) buffers through the C ABI, copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if args.seeding:
+        e2e = {"skipped": "seeding mode draws the candidates on the device"}
+    elif not args.no_e2e:
         ids_h = torch.from_numpy(J.view(np.int32)).pin_memory()
         grad_h = grad.cpu().pin_memory()
         out_h = torch.empty(world * cfg.K, dtype=torch.int32).pin_memory()
@@ -475,7 +499,7 @@ def main():
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not args.seeding:
         tps, desc, n, dt = oracle_sample(cfg, 1, args.mode, args.cpu_seconds)
         cpu = {"value": tps, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                "host_cores_available": host_cores()}
@@ -491,6 +515,7 @@ def main():
                 "U_local": info.get("u_local"), "U_global": ug, "E_U_global_closed_form": eu,
                 "phases_us_diagnostic": ph, "roofline": roof, "roofline_s5_s6": upd,
                 "dense_baseline": dense, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+                "seed_plan": seed_plan,
                 "gpu_launches": sync_launches, "gpu_launches_per_step": sync_launches / args.steps,
                 "step_us_per_rank": all_ms if world > 1 else [[round(1e3 * x, 1) for x in ms]],
                 "library": lmscale.version()}

@@ -279,6 +279,35 @@ LMSCALE_API lmscale_status lmscale_compress(lmscale_ctx* ctx, const float* x, in
 LMSCALE_API lmscale_status lmscale_decompress(lmscale_ctx* ctx, const uint16_t* q, int64_t n,
                                               float F, float* x, void* stream);
 
+/* Seeding (Sec. 3.2; reading R16).  Sampled softmax
+ * picks S candidate words per GPU (1024 in the paper); GPUs that share
+ * a seed draw the same words, so the output-embedding exchange over
+ * [K targets || S samples] keeps a small global unique set.  Policies: */
+#define LMSCALE_SEED_DISTINCT 0 /* every GPU its own seed (G groups) */
+#define LMSCALE_SEED_SAME 1     /* one seed for all (1 group) */
+#define LMSCALE_SEED_LOG2 2     /* max(1, round(log2 G)) groups */
+#define LMSCALE_SEED_LOGE 3     /* max(1, round(ln G)) groups */
+#define LMSCALE_SEED_LOG10 4    /* max(1, round(log10 G)) groups */
+#define LMSCALE_SEED_POWER 5    /* max(1, ceil(G^alpha)) groups, 0 < alpha <= 1 (0.64) */
+
+/* Host only (no GPU, no context): seeds_out[r] (host, world entries) = the
+ * seed of rank r.  Ranks form contiguous near-equal blocks, group(r) =
+ * floor(r * n / world); seed of group q = SplitMix64 output of master + q.
+ * *groups_out (host, may be NULL) = n.  INVALID_ARG: world < 1, unknown
+ * policy, alpha outside (0, 1] for POWER, NULL seeds_out. */
+LMSCALE_API lmscale_status lmscale_plan_seeds(int32_t world, int32_t policy, double alpha,
+                                              uint64_t master_seed, uint64_t* seeds_out,
+                                              int32_t* groups_out);
+
+/* Draw S candidate ids (device, S uint32 written to out) uniformly without
+ * replacement from [0, vocab): the first S distinct values of the stream
+ * x_i = floor(u_i * vocab / 2^64), u_i = mix64(A + i), A = mix64(seed ^
+ * mix64(step)) (R16), in stream order.  Deterministic per (seed, step, S,
+ * vocab); ranks with the same seed and step get the same ids.  One CTA,
+ * stream-ordered.  INVALID_ARG: S < 1, S > vocab, S > 8192, out NULL. */
+LMSCALE_API lmscale_status lmscale_draw_samples(lmscale_ctx* ctx, uint64_t seed, uint64_t step,
+                                                int64_t S, uint32_t* out, void* stream);
+
 LMSCALE_API lmscale_status lmscale_get_stats(const lmscale_ctx* ctx, lmscale_stats* out /* host */);
 LMSCALE_API const char* lmscale_status_string(lmscale_status s);
 /* Last detailed error message of this context (static storage inside ctx). */

@@ -283,13 +283,21 @@ size_t cluster_smem_bytes(int bits) {
   return (size_t)(4 * CL_MAX_TILE + (NW + 4) * (1 << bits) + 32) * 4;
 }
 
-static int cluster_items(int K) { return K <= CL_MAX_CTAS * CL_THREADS * 4 ? 4 : 8; }
+// keys per thread: the fewest that fit K into one cluster of <= CL_MAX_CTAS CTAs
+// (K just above 32K -- e.g. the 32768 + 1024 ids of the seeded output
+// exchange -- keeps 16 CTAs instead of dropping to 9 CTAs x 8 keys)
+static int cluster_items(int K) {
+  for (int it : {4, 5, 6})
+    if (K <= CL_MAX_CTAS * CL_THREADS * it) return it;
+  return 8;
+}
 
 bool cluster_s1_ok(int K) {
   static int ok = -1;
   if (ok < 0) {
     ok = 1;
-    for (const void* f : {(const void*)k_s1_cluster<4>, (const void*)k_s1_cluster<8>}) {
+    for (const void* f : {(const void*)k_s1_cluster<4>, (const void*)k_s1_cluster<5>,
+                          (const void*)k_s1_cluster<6>, (const void*)k_s1_cluster<8>}) {
       ok &= cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                 cudaSuccess &&
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -317,8 +325,12 @@ cudaError_t launch_s1_cluster(const S1Args& a, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return it == 4 ? cudaLaunchKernelEx(&cfg, k_s1_cluster<4>, a)
-                 : cudaLaunchKernelEx(&cfg, k_s1_cluster<8>, a);
+  switch (it) {
+    case 4: return cudaLaunchKernelEx(&cfg, k_s1_cluster<4>, a);
+    case 5: return cudaLaunchKernelEx(&cfg, k_s1_cluster<5>, a);
+    case 6: return cudaLaunchKernelEx(&cfg, k_s1_cluster<6>, a);
+    default: return cudaLaunchKernelEx(&cfg, k_s1_cluster<8>, a);
+  }
 }
 
 }  // namespace lms

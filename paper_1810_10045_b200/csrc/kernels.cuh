@@ -142,6 +142,12 @@ struct ScatterArgs {
 };
 // One cooperative launch: scatter, cut-run fixup, and (a.table) the world-1 S6.
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
+// seeding (Sec. 3.2, R16): the first S distinct draws of the (seed, step) stream
+constexpr int DRAW_MAX_S = 8192;
+cudaError_t launch_draw_samples(uint64_t seed, uint64_t step, int S, uint64_t V, uint32_t* out,
+                                cudaStream_t s);
+// seed-group plan; returns the number of groups, -1 on a bad policy / alpha
+int plan_seed_groups(int world, int policy, double alpha, uint64_t master, uint64_t* seeds);
 // compression codec (R15): down = compress (fp32 -> binary16 bits), else decompress
 cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* out, int num_sms,
                          cudaStream_t s);

@@ -437,6 +437,30 @@ lmscale_status lmscale_decompress(lmscale_ctx* ctx, const uint16_t* q, int64_t n
   return codec_call(ctx, false, q, n, F, x, stream);
 }
 
+lmscale_status lmscale_plan_seeds(int32_t world, int32_t policy, double alpha,
+                                  uint64_t master_seed, uint64_t* seeds_out,
+                                  int32_t* groups_out) {
+  if (world < 1 || !seeds_out) return LMSCALE_ERR_INVALID_ARG;
+  const int n = plan_seed_groups(world, policy, alpha, master_seed, seeds_out);
+  if (n < 1) return LMSCALE_ERR_INVALID_ARG;
+  if (groups_out) *groups_out = n;
+  return LMSCALE_OK;
+}
+
+lmscale_status lmscale_draw_samples(lmscale_ctx* ctx, uint64_t seed, uint64_t step, int64_t n,
+                                    uint32_t* out, void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (!out || n < 1 || n > ctx->cfg.vocab || n > DRAW_MAX_S)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "draw_samples: S=%lld (vocab %lld, max %d)",
+                (long long)n, (long long)ctx->cfg.vocab, DRAW_MAX_S);
+  cudaSetDevice(ctx->cfg.device);
+  begin_call(ctx);
+  CK(launch_draw_samples(seed, step, (int)n, (uint64_t)ctx->cfg.vocab, out, S(stream)));
+  LAUNCHED(1);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
 lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return LMSCALE_ERR_INVALID_ARG;
   if (mode != ctx->tmode && ctx->gexec) {  // the captured graph carries the old events

@@ -82,6 +82,11 @@ _host_step = _sig("lmscale_train_step_host", _S,
                   [_P, _P, _P, _i64, _P, ctypes.c_float, _P, ctypes.POINTER(_i64), _P])
 _alloc_table = _sig("lmscale_alloc_table", _S, [_P, ctypes.POINTER(_P), ctypes.POINTER(_i64)])
 _set_timing = _sig("lmscale_set_timing", _S, [_P, ctypes.c_int])
+_plan_seeds = _sig("lmscale_plan_seeds", _S, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                                ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64),
+                                                ctypes.POINTER(ctypes.c_int32)])
+_draw_samples = _sig("lmscale_draw_samples", _S, [_P, ctypes.c_uint64, ctypes.c_uint64, _i64, _P,
+                                                  _P])
 _set_compression = _sig("lmscale_set_compression", _S, [_P, ctypes.c_float])
 _compress = _sig("lmscale_compress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
 _decompress = _sig("lmscale_decompress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
@@ -95,8 +100,23 @@ EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_u
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
             "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
             "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing", "lmscale_alloc_table",
-            "lmscale_set_compression", "lmscale_compress", "lmscale_decompress", "lmscale_get_stats",
+            "lmscale_set_compression", "lmscale_compress", "lmscale_decompress",
+            "lmscale_plan_seeds", "lmscale_draw_samples", "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
+
+
+SEED_POLICIES = {"distinct": 0, "same": 1, "log2": 2, "loge": 3, "log10": 4, "power": 5}
+
+
+def plan_seeds(world: int, policy: str = "power", alpha: float = 0.64, master_seed: int = 0):
+    """Sec. 3.2 seed groups (host only): (seeds per rank, number of groups)."""
+    seeds = (ctypes.c_uint64 * world)()
+    n = ctypes.c_int32()
+    st = _plan_seeds(int(world), SEED_POLICIES[policy], float(alpha),
+                     int(master_seed) & (2**64 - 1), seeds, ctypes.byref(n))
+    if st != OK:
+        raise LmscaleError(st, f"lmscale_plan_seeds({world}, {policy}, {alpha})")
+    return [int(x) for x in seeds], int(n.value)
 
 
 class LmscaleError(RuntimeError):
@@ -336,6 +356,16 @@ class Context:
         self._check(_decompress(self._h, _ptr(q), q.numel(), float(F), _ptr(x), _stream(stream)),
                     "lmscale_decompress")
         return x
+
+    def draw_samples(self, seed: int, step: int, S: int, out=None, stream=None) -> torch.Tensor:
+        """Sec. 3.2 candidates: S distinct ids of the (seed, step) stream (R16),
+        as an int32 view of the uint32 ids; written into `out` when given."""
+        if out is None:
+            out = torch.empty(S, dtype=torch.int32, device=self.device)
+        assert out.is_cuda and out.numel() >= S and out.element_size() == 4 and out.is_contiguous()
+        self._check(_draw_samples(self._h, int(seed) & (2**64 - 1), int(step) & (2**64 - 1), int(S),
+                                  _ptr(out), _stream(stream)), "lmscale_draw_samples")
+        return out[:S]
 
     def stats(self) -> dict:
         s = StatsC()

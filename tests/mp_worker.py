@@ -175,6 +175,40 @@ def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
     ctx.close()
 
 
+def run_seeded(cfg, rank, G, dev, policy, S=1024, mode="int"):
+    """Sec. 3.2 output-embedding exchange: every rank draws S candidates with
+    its group's seed (lmscale_plan_seeds + lmscale_draw_samples, R16) into the
+    tail of [K targets || S samples] and runs lmscale_step; checked against
+    the oracle's plan, draws and seven-step exchange over every rank's list."""
+    lr = synth.default_lr(mode)
+    seeds, ngroups = lmscale.plan_seeds(G, policy, 0.64, master_seed=181010045)
+    oseeds, on = oracle.plan_seeds(G, policy, alpha=0.64, master_seed=181010045)
+    assert (seeds, ngroups) == (oseeds, on)
+    step = 3
+    ctx = make_context(cfg.V, cfg.K + S, cfg.D)
+    J = torch.empty(cfg.K + S, dtype=torch.int32, device=dev)
+    J[:cfg.K] = torch.from_numpy(synth.ids_for(cfg, rank).view(np.int32)).to(dev)
+    ctx.draw_samples(seeds[rank], step, S, out=J[cfg.K:])
+    Dh = [synth.grad_values(cfg.K + S, cfg.D, mode, rank=g) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, mode)
+    E = E0.to(dev)
+    ug = ctx.step(J, Dh[rank].to(dev), E, lr, want_num_unique=True)
+    torch.cuda.synchronize()
+    Jall = [np.concatenate([synth.ids_for(cfg, g), oracle.draw_samples(oseeds[g], step, S, cfg.V)])
+            for g in range(G)]
+    np.testing.assert_array_equal(u32(J), Jall[rank])
+    Eo = E0.numpy().copy()
+    ref = oracle.sync_unique(Jall, [d.numpy() for d in Dh], Eo, lr)
+    assert ug == ref["Ug"]
+    if mode == "int":
+        np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+    check_replicas(E, f"seeded {policy}")
+    if rank == 0:
+        print(f"seeded G={G} {cfg.name} policy={policy} groups={ngroups} U_g={ug}", flush=True)
+    ctx.close()
+    return ug
+
+
 def compressed_row(Js, Ds, w, F):
     """Oracle M^ row of one word under compression, from the definition: each
     rank's M_g row is the fp64 sum of its Delta rows of that word, rounded to
@@ -257,6 +291,10 @@ def main():
         run_fused_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
         for mode in ("int", "signed"):
             run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev, own_table=True)
+    if "seed" in which:
+        ugs = {p: run_seeded(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev, p, S=512)
+               for p in ("distinct", "power", "same")}
+        assert ugs["same"] <= ugs["power"] <= ugs["distinct"]
     if "comp" in which:
         for F in (1.0, 1024.0):
             run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "int", rank, G, dev, F)

@@ -61,3 +61,17 @@ def test_sm100a_code_in_library(lib):
     _, path = lib
     out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("policy", ["distinct", "same", "log2", "loge", "log10", "power"])
+def test_plan_seeds_host_logic_matches_oracle(lib, policy):
+    """lmscale_plan_seeds is host-only (no GPU): same groups and seeds as the
+    oracle's plan for every G up to 130 (Sec. 3.2, R16)."""
+    import oracle
+    from paper_1810_10045_b200 import lmscale
+    for G in list(range(1, 70)) + [100, 128, 130]:
+        got = lmscale.plan_seeds(G, policy, 0.64, master_seed=181010045)
+        want = oracle.plan_seeds(G, policy, alpha=0.64, master_seed=181010045)
+        assert got == (want[0], want[1]), (G, policy)
+    with pytest.raises(lmscale.LmscaleError):
+        lmscale.plan_seeds(8, "power", 1.5)

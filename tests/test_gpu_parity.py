@@ -51,6 +51,9 @@ UNIQUE_CASES = [
     ("2^32-1 vocab", 2**32 - 1, np.random.default_rng(2).integers(0, 2**32 - 1, 9000,
                                                                    dtype=np.uint64).astype(np.uint32)),
     ("ragged-tail", 50_000, synth.zipf_ids(50_000, 1.0, 4096 * 3 + 17)),
+    ("cluster-5-keys", 793_000, synth.zipf_ids(793_000, 1.0, 32768 + 1024)),
+    ("cluster-6-keys", 793_000, synth.zipf_ids(793_000, 1.0, 45_001)),
+    ("cluster-8-keys", 793_000, synth.zipf_ids(793_000, 1.0, 60_000)),
 ]
 
 
@@ -458,4 +461,27 @@ def test_step_with_bad_id_leaves_table_untouched(lm):
     ctx.step(to_dev_ids(np.array([1, 2, 2, 3], np.uint32)), torch.ones(4, 8, device=dev()), E, 0.5)
     torch.cuda.synchronize()
     assert E[2, 0].item() == 0.0 and E[1, 0].item() == 0.5 and E[0, 0].item() == 1.0
+    ctx.close()
+
+
+# ------------------------------------------------------------ seeding (3.2)
+
+@pytest.mark.parametrize("seed,step,S,V", [
+    (0, 0, 1, 1), (1, 2, 10, 10), (7, 3, 1024, 793_000), (181010045, 11, 1024, 2_000_000),
+    (5, 1, 8192, 500_000), (9, 9, 3000, 3000), (3, 4, 1500, 2**32 - 1), (4, 5, 2048, 2100)])
+def test_draw_samples_bit_exact(lm, seed, step, S, V):
+    """lmscale_draw_samples == the oracle's first-S-distinct stream (R16),
+    element by element in stream order."""
+    ctx = lm.Context(V, 16, 4)
+    got = ctx.draw_samples(seed, step, S)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(host_u32(got), oracle.draw_samples(seed, step, S, V))
+    ctx.close()
+
+
+def test_draw_samples_rejects_bad_sizes(lm):
+    ctx = lm.Context(100, 16, 4)
+    for S in (0, 101, 9000):
+        with pytest.raises(lm.LmscaleError):
+            ctx.draw_samples(1, 1, S)
     ctx.close()

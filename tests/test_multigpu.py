@@ -81,3 +81,13 @@ def test_compressed_exchange_matches_oracle(n):
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     _torchrun(n, ["comp"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 4])
+def test_seeded_output_exchange_matches_oracle(n):
+    """Sec. 3.2 seeding on real GPUs: plans, draws and the exchange over
+    [targets || samples] bit-exact (INT mode) against the oracle."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    _torchrun(n, ["seed"])
