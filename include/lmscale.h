@@ -72,7 +72,9 @@ typedef enum {
 #define LMSCALE_FLAG_TIMING 2u  /* record CUDA events around each phase; lmscale_get_stats reports them */
 #define LMSCALE_FLAG_GRAPH 4u   /* lmscale_step captures the whole step into a CUDA graph (once per
                                    (ids, grad, table, k, lr) tuple) and replays it; applies with
-                                   world == 1 and num_unique_out == NULL (no host round trip) */
+                                   num_unique_out == NULL (no host round trip) and either
+                                   world == 1 or a world > 1 context with the symmetric window
+                                   (peer-bitmap S3 + fused S5+S6: no NCCL host calls) */
 
 typedef struct {
   int64_t vocab;      /* |V| >= 1 */

@@ -327,6 +327,42 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   const int64_t gthreads = (int64_t)gridDim.x * CT;
 
   stamp(a.trace, 32);
+  if (a.peer_mode) {
+    // handshake: this rank's S1 (the previous kernel on this stream) is
+    // complete; tell every peer, then wait until every peer has said so
+    // (flag = 2 * epoch + this rank's id-error bit: every rank learns every
+    // rank's error, so all of them report it and none enters a collective alone)
+    if (gtid == 0) {
+      const uint32_t e = *a.epoch + 1u;
+      *a.epoch = e;
+      const uint32_t f = 2u * e + (__ldcg(&a.sc1->err) & 1u);
+      __threadfence_system();
+      for (int j = 0; j < a.world; ++j)
+        st_release_sys(reinterpret_cast<uint32_t*>(a.peer_base[j] + a.flags_off) + a.rank, f);
+      const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.peer_base[a.rank] + a.flags_off);
+      uint32_t err = 0u;
+      for (int j = 0; j < a.world; ++j) {
+        uint32_t v;
+        while ((int32_t)((v = ld_acquire_sys(mine + j)) - 2u * e) < 0) __nanosleep(64);
+        err |= v & 1u;
+      }
+      a.sc->err = err;
+      a.sc->u_global = 0;
+    }
+    grid_barrier(a.bar);
+    stamp(a.trace, 33);
+    // phase A': the global presence bitmap = OR of the G local bitmaps
+    for (int64_t w = gtid; w < a.W; w += gthreads) {
+      uint32_t g = 0u;
+#pragma unroll 8
+      for (int j = 0; j < a.world; ++j)
+        g |= __ldcv(reinterpret_cast<const uint32_t*>(a.peer_base[j] + a.lbits_off) + w);
+      a.gbits[w] = g;
+    }
+    stamp(a.trace, 35);
+    grid_barrier(a.bar);
+    stamp(a.trace, 36);
+  } else {
   // phase 0: zero the bitmap and scalars
   for (int64_t w = gtid; w < a.W; w += gthreads) a.gbits[w] = 0u;
   if (gtid == 0) {
@@ -382,6 +418,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   stamp(a.trace, 35);
   grid_barrier(a.bar);
   stamp(a.trace, 36);
+  }  // !peer_mode
 
   // phase B: popcounts of this CTA's word range (one word per thread per round)
   const int64_t per = (a.W + gridDim.x - 1) / gridDim.x;
@@ -509,7 +546,8 @@ cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s) {
   }
   // enough CTAs for the id and word volumes, few enough that barriers stay cheap
   int64_t want = (a.n + 4095) / 4096;
-  const int64_t ww = (a.W + 2047) / 2048;
+  // peer mode: one remote word per thread per peer in the OR phase
+  const int64_t ww = a.peer_mode ? (a.W + CO_THREADS - 1) / CO_THREADS : (a.W + 2047) / 2048;
   if (ww > want) want = ww;
   if (want < 1) want = 1;
   const int64_t cap = (int64_t)num_sms * occ;

@@ -87,6 +87,15 @@ struct S3Args {
   int32_t* l2g;
   unsigned long long* trace;
   GridBar* bar;
+  // peer mode (the J^-set exchange): instead of building
+  // the bitmap from a gathered I, OR the G local presence bitmaps (S1's lbits)
+  // read from the peers' symmetric windows after a flag handshake
+  int peer_mode;
+  int world, rank;
+  char* peer_base[8];   // LSA base of each rank's M window
+  size_t lbits_off;     // byte offset of lbits in the window
+  size_t flags_off;     // byte offset of the per-rank arrival flags (world words)
+  uint32_t* epoch;      // local step counter of the handshake (device)
 };
 SortPlan make_coop_plan(uint64_t vocab);
 
@@ -174,6 +183,8 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
                         float cF, size_t mhat_off, cudaStream_t s);
 // true: the peer-to-peer fused kernel (presence-aware) is used for this G
 bool nvls_use_p2p(int world);
+// LSA base of every rank's M window (world entries written to out_host)
+bool nvls_peer_bases(NvlsState* st, int world, void** out_host);
 ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,
                                  size_t errlen);
 void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w);

@@ -70,6 +70,10 @@ struct lmscale_ctx {
   NvlsState* nvls = nullptr;   // fused S5+S6 available
   size_t lbits_off = 0;        // byte offset of lbits inside the M window
   size_t mhat_off = 0;         // byte offset of the compressed M^ rows inside the M window
+  size_t flags_off = 0;        // byte offset of the S3 handshake flags inside the M window
+  char* peer_base[8] = {};     // LSA base of every rank's M window
+  bool peer_s3 = false;        // S3 ORs the peers' local bitmaps (no ID all-gather)
+  uint32_t* s3_epoch = nullptr;
   float cF = 0.f;              // compression scale (0: off), lmscale_set_compression
   GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
   float* table_ptr = nullptr;  // lmscale_alloc_table
@@ -237,8 +241,16 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
 
 // S3 on stream s: one cooperative launch (bitmap, scan, I^, U_g,
 // and the l2g map of the last S1, which must be complete on `s`).
-lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream_t s) {
+lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream_t s,
+                      bool peer = false) {
   S3Args a;
+  a.peer_mode = peer ? 1 : 0;
+  a.world = ctx->cfg.world;
+  a.rank = ctx->cfg.rank;
+  for (int j = 0; j < 8; ++j) a.peer_base[j] = ctx->peer_base[j];
+  a.lbits_off = ctx->lbits_off;
+  a.flags_off = ctx->flags_off;
+  a.epoch = ctx->s3_epoch;
   a.I = I;
   a.n = n;
   a.vocab = (uint32_t)ctx->cfg.vocab;
@@ -523,7 +535,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
            o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
            o_bT = take(4 * (size_t)ctx->ntiles_max * (1u << ctx->plan.bits)),
-           o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W);
+           o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W), o_epoch = take(64);
     // M lives in its own allocation: with a communicator it comes from
     // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
     // (+256: room to align the compressed M^ region at byte 2*ucap*D)
@@ -560,6 +572,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->ctot = (uint32_t*)(b + o_ctot);
     ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
+    ctx->s3_epoch = (uint32_t*)(b + o_epoch);
     ctx->partial = (float*)(b + o_part);
     ctx->part2 = (float*)(b + o_part2);
     CK(cudaMemset(ctx->base, 0, off));
@@ -583,7 +596,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       // M and this rank's local presence bitmap share one symmetric window:
       // the fused kernel reads the peers' bitmaps to load only present rows
       const size_t lb_off = m_bytes;
-      const size_t win_bytes = align_up(m_bytes + 4 * (size_t)ctx->W, 1 << 21);
+      const size_t fl_off = align_up(m_bytes + 4 * (size_t)ctx->W, 256);
+      const size_t win_bytes = align_up(fl_off + 4 * 64, 1 << 21);
       void* m = nullptr;
       if (ncclMemAlloc(&m, win_bytes) != ncclSuccess)
         return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(%zu) failed", win_bytes);
@@ -599,6 +613,9 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       if (ctx->nvls) {
         ctx->lbits = (uint32_t*)((char*)m + lb_off);
         ctx->lbits_off = lb_off;
+        ctx->flags_off = fl_off;
+        ctx->peer_s3 = !getenv("LMSCALE_NO_PEER_S3") && cfg->world <= 8 &&
+                       nvls_peer_bases(ctx->nvls, cfg->world, (void**)ctx->peer_base);
       } else {
         snprintf(ctx->nvls_why, sizeof(ctx->nvls_why), "%s", why);
         NK(ncclCommRegister(ctx->comm, ctx->M, win_bytes, &ctx->m_reg));
@@ -786,7 +803,16 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   if (ctx->trace && !ctx->capturing) cudaMemsetAsync(ctx->trace, 0, 64 * sizeof(unsigned long long), s);
   const uint32_t* I = ids;
   int64_t n = k;
-  if (G > 1) {
+  const bool peer_s3 = G > 1 && ctx->peer_s3;
+  if (peer_s3) {
+    // J^-set exchange: no ID all-gather; S3 ORs the G
+    // local presence bitmaps over NVLink after S1 (same I^, U_g and l2g).
+    rec(ctx, EV_S1_BEGIN, s);
+    st = run_s1(ctx, ids, k, nullptr, s);
+    if (st) return st;
+    rec(ctx, EV_S1_END, s);
+    rec(ctx, EV_GATHER_END, s);
+  } else if (G > 1) {
     // S1 on the side stream, concurrent with the S2 ID all-gather.
     CK(cudaEventRecord(ctx->ev_fork, s));
     CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_fork, 0));
@@ -811,7 +837,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   rec(ctx, EV_JOIN, s);
   // S3: I^, U_g, l2g; {U_g, err, U_i} to the host on the copy stream.
   if (G > 1) {
-    st = run_s3(ctx, I, n, s);
+    st = peer_s3 ? run_s3(ctx, nullptr, 0, s, true) : run_s3(ctx, I, n, s);
     if (st) return st;
   }
   rec(ctx, EV_S3_END, s);
@@ -963,11 +989,12 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
 lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* grad, int64_t k,
                             float* table, float lr, int64_t* num_unique_out, void* stream) {
   if (ctx && !table) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "table is NULL");
-  // CUDA-graph replay: the step has no host round trip when world == 1 or the
-  // fused NVLS kernel is available, so it is captured once per argument tuple
-  // and replayed (one launch instead of ~5 kernels + events + NCCL calls).
+  // CUDA-graph replay: the step has no host round trip when world == 1, or
+  // when world > 1 runs the peer-bitmap S3 and a fused S5+S6 kernel (no NCCL
+  // host calls at all), so it is captured once per argument tuple and
+  // replayed (one launch instead of 3-4 kernels + events).
   if (ctx && (ctx->cfg.flags & LMSCALE_FLAG_GRAPH) && !num_unique_out &&
-      ctx->cfg.world == 1) {
+      (ctx->cfg.world == 1 || (ctx->peer_s3 && ctx->nvls))) {
     lmscale_status st0 = check_ids_args(ctx, ids, k);
     if (st0) return st0;
     cudaStream_t s = S(stream);

@@ -410,6 +410,22 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st) {
   delete st;
 }
 
+__global__ void k_peer_bases(ncclWindow_t win, int world, void** out) {
+  if ((int)threadIdx.x < world) out[threadIdx.x] = ncclGetLsaPointer(win, 0, (int)threadIdx.x);
+}
+
+// LSA base address of every rank's M window (plain device pointers over
+// NVLink), for kernels outside this file that read peer memory directly.
+bool nvls_peer_bases(NvlsState* st, int world, void** out_host) {
+  void** d = nullptr;
+  if (cudaMalloc(&d, 8 * sizeof(void*)) != cudaSuccess) return false;
+  k_peer_bases<<<1, 32>>>(st->win, world, d);
+  const bool ok = cudaMemcpy(out_host, d, world * sizeof(void*), cudaMemcpyDeviceToHost) ==
+                  cudaSuccess;
+  cudaFree(d);
+  return ok;
+}
+
 bool nvls_use_p2p(int world) {
   static const int p2p_max =
       getenv("LMSCALE_P2P_MAX_G") ? atoi(getenv("LMSCALE_P2P_MAX_G")) : 8;

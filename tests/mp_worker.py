@@ -124,6 +124,35 @@ def run_fused_small(cfg, mode, rank, G, dev, own_table=False):
     ctx.close()
 
 
+def run_graph_equals_eager(cfg, rank, G, dev, F=0.0):
+    """World > 1 with LMSCALE_FLAG_GRAPH (peer-bitmap S3 + fused S5+S6, no NCCL
+    host calls): three captured-and-replayed steps give the same table bits as
+    three eager steps, new buffer contents included."""
+    mode = "signed"
+    lr = synth.default_lr(mode)
+    ids = torch.from_numpy(synth.ids_for(cfg, rank).view(np.int32)).to(dev)
+    g = synth.grad_values(cfg.K, cfg.D, mode, rank=rank).to(dev)
+    outs = []
+    for flags in (0, lmscale.FLAG_GRAPH):
+        ctx = make_context(cfg.V, cfg.K, cfg.D, flags=flags)
+        if F > 0:
+            ctx.set_compression(F)
+        E = ctx.alloc_table()
+        E.copy_(synth.table_values(cfg.V, cfg.D, mode).to(dev))
+        ids_b, g_b = ids.clone(), g.clone()
+        for t in range(3):
+            if t == 2:
+                ids_b.copy_(torch.from_numpy(synth.ids_for(cfg, rank, step=1).view(np.int32)).to(dev))
+            ctx.step(ids_b, g_b, E, lr)
+        torch.cuda.synchronize()
+        outs.append(E.clone())
+        check_replicas(E, f"graph={flags} {cfg.name}")
+        ctx.close()
+    assert torch.equal(outs[0], outs[1]), "graph replay differs from eager"
+    if rank == 0:
+        print(f"graph==eager G={G} {cfg.name} F={F}", flush=True)
+
+
 def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
     """lmscale_step with compression (Sec. 3.3, R15) against
     oracle.sync_unique_compressed: INT mode bit-exact over the whole table,
@@ -291,6 +320,9 @@ def main():
         run_fused_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
         for mode in ("int", "signed"):
             run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev, own_table=True)
+    if "small" in which or "graph" in which:
+        run_graph_equals_eager(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev)
+        run_graph_equals_eager(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev, F=1.0)
     if "seed" in which:
         ugs = {p: run_seeded(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev, p, S=512)
                for p in ("distinct", "power", "same")}
