@@ -132,6 +132,9 @@ struct ScatterArgs {
   int2* fixent;           // fix-up entries: (owner chunk, part | nparts << 16)
   float* part2;           // level-2 partial rows, one per entry (fix_cap x D)
   int fix_cap;
+  int fx_last;            // 1: last-arriver fix-up (no grid barrier); 0: listed fix-up phase
+  uint32_t* fxcnt;        // last-arriver counters: parts [fx_stride], runs [fx_stride]
+  int64_t fx_stride;      // nchunks x column blocks
   int zero_rows;          // 0: every slot is present locally (world 1): slot = local index
   int fill_absent;        // zero the M rows of slots absent on this rank (world > 1)
   int m16;                // M rows are stored compressed (binary16 of cF * x, R15)

@@ -62,6 +62,8 @@ struct lmscale_ctx {
   uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot, *bT;
   int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
   int2* fixent;
+  uint32_t* fxcnt = nullptr;
+  int64_t fx_stride = 0;
   float* part2;
   float* M = nullptr;
   float* partial;
@@ -313,6 +315,10 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fixent = ctx->fixent;
   a.part2 = ctx->part2;
   a.fix_cap = (int)(2 * ctx->nchunks);
+  static const bool fx_barrier = getenv("LMSCALE_S4_FIXUP_BARRIER") != nullptr;
+  a.fx_last = fx_barrier ? 0 : 1;
+  a.fxcnt = ctx->fxcnt;
+  a.fx_stride = ctx->fx_stride;
   a.zero_rows = ctx->cfg.world > 1 ? 1 : 0;  // world 1: slot = local index
   a.fill_absent = 1;
   a.m16 = 0;
@@ -543,6 +549,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->mhat_off = align_up(2 * (size_t)ctx->ucap * D, 256);
     size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
     size_t o_part2 = take(4 * (size_t)2 * ctx->nchunks * D);
+    ctx->fx_stride = 2 * ctx->nchunks * ((D + 127) / 128 + 1);
+    size_t o_fxcnt = take(4 * 2 * (size_t)ctx->fx_stride);
     ctx->ws_bytes = off;
     if (cudaMalloc(&ctx->base, off) != cudaSuccess) {
       cudaGetLastError();
@@ -575,6 +583,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->s3_epoch = (uint32_t*)(b + o_epoch);
     ctx->partial = (float*)(b + o_part);
     ctx->part2 = (float*)(b + o_part2);
+    ctx->fxcnt = (uint32_t*)(b + o_fxcnt);
     CK(cudaMemset(ctx->base, 0, off));
     CK(cudaHostAlloc((void**)&ctx->h_sc3, sizeof(Sc3) + sizeof(Sc1), cudaHostAllocDefault));
     ctx->h_sc1 = (Sc1*)((char*)ctx->h_sc3 + sizeof(Sc3));

@@ -122,7 +122,98 @@ __device__ __forceinline__ void emit_row(const ScatterArgs& a, size_t slot, uint
 // Only long runs (the Zipf head) are cut into partial rows (P[2c] head piece,
 // P[2c+1] tail piece) and listed for the fix-up phase by the chunk holding
 // their start.  FULLC: the column block lies inside the row (no predicates).
-template <typename T, int NV, int UNR, bool FULLC, bool PRE>
+// ---- last-arriver fix-up of runs cut by chunk boundaries (no grid barrier)
+// A run spanning chunks c0..c1 leaves np = c1 - c0 + 1 partial rows: k = 0 is
+// the tail piece of c0 (P[2c0+1]), k >= 1 the head piece of c0+k (P[2(c0+k)]).
+// They are summed in parts of FXP partials: the warp that stores the last
+// partial of a part (atomic counter per (part, column block)) sums that part
+// in k order; with one part it emits the row, else it stores a level-2 row
+// and the last part to finish sums the level-2 rows in part order.  Fixed
+// summation order: deterministic.  Counters reset themselves for the next
+// launch.
+constexpr int FXP = 32;
+
+// partial rows k in [k0, k0 + n) of the run starting at chunk c0, summed in k order
+template <typename T, int NV>
+__device__ __forceinline__ void sum_partials(const T* base, int c0, int k0, int n, int col0, int C,
+                                             T (&acc)[NV]) {
+  using V = Vec<T>;
+  constexpr int FU = NV >= 4 ? 2 : 4;  // rows in flight (register budget of the 4-vector path)
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+  for (int i = 0; i < n; i += FU) {
+    T r[FU][NV];
+#pragma unroll
+    for (int q = 0; q < FU; ++q) {
+      const int kk = k0 + i + q;
+      const size_t row = kk == 0 ? (size_t)(2 * c0 + 1) : (size_t)(2 * (c0 + kk));
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int col = col0 + v * 32;
+        r[q][v] = V::zero();
+        if (i + q < n && col < C) r[q][v] = V::ld_l2(base + row * C + col);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < FU; ++q)
+      if (i + q < n)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r[q][v]);
+  }
+}
+
+template <typename T, int NV>
+__device__ __forceinline__ void fix_arrive(const ScatterArgs& a, int u, int c0, int k, int np, int cb,
+                                        int ncb, int col0, int C, int lane) {
+  using V = Vec<T>;
+  uint32_t* pcnt = a.fxcnt;
+  uint32_t* rcnt = a.fxcnt + a.fx_stride;
+  const int j = k / FXP, nparts = (np + FXP - 1) / FXP;
+  // ids of a part / a run = the partial-row index of its first piece (unique:
+  // every partial row belongs to exactly one run): counter and level-2 row
+  const int pc = j == 0 ? 2 * c0 + 1 : 2 * (c0 + j * FXP);
+  const int rc = 2 * c0 + 1;
+  const int cnt = min(FXP, np - j * FXP);
+  __syncwarp();
+  __threadfence();
+  uint32_t old = 0;
+  if (lane == 0) old = atomicAdd(pcnt + (size_t)pc * ncb + cb, 1u);
+  old = __shfl_sync(FULL_MASK, old, 0);
+  if ((int)old != cnt - 1) return;
+  if (lane == 0) pcnt[(size_t)pc * ncb + cb] = 0u;
+  __threadfence();
+  T acc[NV];
+  sum_partials<T, NV>(reinterpret_cast<const T*>(a.partial), c0, j * FXP, cnt, col0, C, acc);
+  if (nparts > 1) {
+    T* L2 = reinterpret_cast<T*>(a.part2) + (size_t)pc * C;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (col0 + v * 32 < C) V::st(L2 + col0 + v * 32, acc[v]);
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) old = atomicAdd(rcnt + (size_t)rc * ncb + cb, 1u);
+    old = __shfl_sync(FULL_MASK, old, 0);
+    if ((int)old != nparts - 1) return;
+    if (lane == 0) rcnt[(size_t)rc * ncb + cb] = 0u;
+    __threadfence();
+    const T* L2b = reinterpret_cast<const T*>(a.part2);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+    for (int jj = 0; jj < nparts; ++jj)
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        if (col0 + v * 32 < C)
+          acc[v] = V::add(acc[v], V::ld_l2(L2b + (size_t)(jj == 0 ? 2 * c0 + 1
+                                                                  : 2 * (c0 + jj * FXP)) * C +
+                                           col0 + v * 32));
+  }
+  const int slot = a.zero_rows ? __ldcg(a.l2g + u) : u;
+  if (slot < 0) return;
+  const uint32_t w = a.apply ? __ldg(a.ihat + slot) : 0u;
+  emit_row<T, NV, false>(a, (size_t)slot, w, C, col0, acc);
+}
+
+template <typename T, int NV, int UNR, bool FULLC, bool PRE, bool FXL>
 __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __restrict__ g,
                                               T* __restrict__ M, T* __restrict__ P, int c,
                                               int n, int col0, int C, int lane) {
@@ -170,6 +261,7 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = V::zero();
   bool seg_first = (p_begin == 0);  // the run being accumulated is the chunk's first
+  bool pend_head = false, pend_tail = false;  // partial rows stored (fix-ups after the loop)
   for (int p0 = p_begin; p0 < p_end; p0 += UNR) {
     T r[UNR][NV];
 #pragma unroll
@@ -216,12 +308,14 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
           T* dst;
           if (seg_first && split_left) {  // long run continuing from the left
             dst = P + (size_t)(2 * c) * C;
+            pend_head = true;
           } else if (last && split_right && last_long) {
             dst = P + (size_t)(2 * c + 1) * C;
+            pend_tail = true;
             // this chunk holds the start of a long run cut by its end: it owns
             // the run's fix-up, listed (by column block 0) as ceil(np / FX_PART)
             // contiguous parts so that the Zipf head is summed by many CTAs
-            if (col0 == lane) {
+            if (!FXL && col0 == lane) {
               int ent = 0, nparts = 0;
               if (lane == 0) {
                 const int np = (l_end - 1) / SC_CHUNK - c + 1;
@@ -260,6 +354,19 @@ __device__ __forceinline__ void scatter_chunk(const ScatterArgs& a, const T* __r
         }
       }
     }
+  }
+  // last-arriver fix-ups of the cut runs this chunk stored pieces of (after
+  // the row loop: no registers of the loop are live across the call)
+  if (FXL && (pend_head || pend_tail)) {
+    const int cb = (col0 - lane) / (32 * NV), ncb = (C + 32 * NV - 1) / (32 * NV);
+    if (pend_head) {
+      const int c0 = f_start / SC_CHUNK;
+      fix_arrive<T, NV>(a, __shfl_sync(FULL_MASK, my_u, 0), c0, c - c0,
+                        (f_end - 1) / SC_CHUNK - c0 + 1, cb, ncb, col0, C, lane);
+    }
+    if (pend_tail)
+      fix_arrive<T, NV>(a, __shfl_sync(FULL_MASK, my_u, n - 1), c, 0,
+                        (l_end - 1) / SC_CHUNK - c + 1, cb, ncb, col0, C, lane);
   }
 }
 
@@ -370,8 +477,8 @@ __device__ __forceinline__ void sstamp(unsigned long long* tr, int i) {
   }
 }
 
-template <typename T, int NV, int UNR, bool PRE>
-__global__ void __launch_bounds__(SC_THREADS, PRE ? 1 : 2) k_scatter(ScatterArgs a) {
+template <typename T, int NV, int UNR, bool PRE, bool FXL>
+__global__ void __launch_bounds__(SC_THREADS, (PRE || FXL) ? 1 : 2) k_scatter(ScatterArgs a) {
   using V = Vec<T>;
   sstamp(a.trace, 54);
   if (a.trace && threadIdx.x == 0) {  // earliest start over all CTAs (as ~t)
@@ -405,9 +512,9 @@ __global__ void __launch_bounds__(SC_THREADS, PRE ? 1 : 2) k_scatter(ScatterArgs
       const int c = (int)unit;
       const int n = min(SC_CHUNK, K - c * SC_CHUNK);
       if ((cb + 1) * 32 * NV <= C)
-        scatter_chunk<T, NV, UNR, true, PRE>(a, g, M, P, c, n, col0, C, lane);
+        scatter_chunk<T, NV, UNR, true, PRE, FXL>(a, g, M, P, c, n, col0, C, lane);
       else
-        scatter_chunk<T, NV, UNR, false, PRE>(a, g, M, P, c, n, col0, C, lane);
+        scatter_chunk<T, NV, UNR, false, PRE, FXL>(a, g, M, P, c, n, col0, C, lane);
     } else {
       // ---- zero rows: slots [r0, r0 + 32) whose word is absent on this rank
       const int64_t r0 = (unit - nchunks) * SC_ZGROUP;
@@ -430,6 +537,8 @@ __global__ void __launch_bounds__(SC_THREADS, PRE ? 1 : 2) k_scatter(ScatterArgs
     }
   }
   sstamp(a.trace, 55);
+  if constexpr (FXL) return;  // cut runs were finished by their last arriving piece
+  if constexpr (!FXL) {
   grid_barrier(a.bar);
   sstamp(a.trace, 56);
 
@@ -449,6 +558,7 @@ __global__ void __launch_bounds__(SC_THREADS, PRE ? 1 : 2) k_scatter(ScatterArgs
     if ((en.y & 0xffff) == 0 && (en.y >> 16) > 1) fixup_final<T, NV>(a, e, (int)(it % ncb), C);
   }
 
+  }
   if (!a.table || a.apply) return;
   grid_barrier(a.bar);
 
@@ -482,12 +592,12 @@ bool vec_ok(const ScatterArgs& a) {
 }
 }  // namespace
 
-template <typename T, int NV, int UNR, bool PRE = false>
+template <typename T, int NV, int UNR, bool PRE = false, bool FXL = false>
 static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   static int occ = 0;  // resident CTAs per SM for this instantiation (persistent grid)
   if (!occ) {
-    max_carveout((const void*)k_scatter<T, NV, UNR, PRE>);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<T, NV, UNR, PRE>, SC_THREADS,
+    max_carveout((const void*)k_scatter<T, NV, UNR, PRE, FXL>);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<T, NV, UNR, PRE, FXL>, SC_THREADS,
                                                       0) != cudaSuccess || occ < 1)
       occ = 1;
   }
@@ -501,7 +611,7 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phases 2/3 want a wide grid
   // grid <= occupancy x SMs: every CTA is co-resident, so the in-kernel
   // grid barrier is safe with a normal launch
-  k_scatter<T, NV, UNR, PRE><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
+  k_scatter<T, NV, UNR, PRE, FXL><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -513,9 +623,19 @@ cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
     // folded S6 at small K (no short-run extension): E rows preloaded per group
     static const bool no_pre = getenv("LMSCALE_NO_PRE") != nullptr;
     if (a.apply && !a.short_runs && !no_pre) {
+      if (a.fx_last) {
+        if (C >= 128) return scatter_t<float4, 4, 4, true, true>(a, s);
+        if (C >= 64) return scatter_t<float4, 2, 4, true, true>(a, s);
+        return scatter_t<float4, 1, 4, true, true>(a, s);
+      }
       if (C >= 128) return scatter_t<float4, 4, 4, true>(a, s);
       if (C >= 64) return scatter_t<float4, 2, 4, true>(a, s);
       return scatter_t<float4, 1, 4, true>(a, s);
+    }
+    if (a.fx_last && !a.short_runs) {  // small K: last-arriver fix-up
+      if (C >= 128) return scatter_t<float4, 4, 4, false, true>(a, s);
+      if (C >= 64) return scatter_t<float4, 2, 4, false, true>(a, s);
+      return scatter_t<float4, 1, 4, false, true>(a, s);
     }
     if (var == 1) return scatter_t<float4, 2, 8>(a, s);
     if (var == 2) return scatter_t<float4, 1, 16>(a, s);
