@@ -310,6 +310,15 @@ LMSCALE_API lmscale_status lmscale_plan_seeds(int32_t world, int32_t policy, dou
 LMSCALE_API lmscale_status lmscale_draw_samples(lmscale_ctx* ctx, uint64_t seed, uint64_t step,
                                                 int64_t S, uint32_t* out, void* stream);
 
+/* Forward lookup: out[p, :] = table[ids[p], :]
+ * for p < k -- the K x dim input activations the gradient rows of the
+ * exchange belong to.  ids: k uint32 (device), table: vocab x dim, out: k x dim
+ * (device, caller-owned).  An id >= vocab yields a zero row (no error is
+ * raised here; lmscale_unique / the step report ID_RANGE).  Stream-ordered,
+ * no communication.  INVALID_ARG: NULL pointers, k < 0. */
+LMSCALE_API lmscale_status lmscale_lookup(lmscale_ctx* ctx, const uint32_t* ids, int64_t k,
+                                          const float* table, float* out, void* stream);
+
 LMSCALE_API lmscale_status lmscale_get_stats(const lmscale_ctx* ctx, lmscale_stats* out /* host */);
 LMSCALE_API const char* lmscale_status_string(lmscale_status s);
 /* Last detailed error message of this context (static storage inside ctx). */

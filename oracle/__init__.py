@@ -88,6 +88,8 @@ def _load():
             lib.oracle_draw_samples.restype = i64
             lib.oracle_draw_samples.argtypes = [ctypes.c_uint64, ctypes.c_uint64, i64,
                                                 ctypes.c_uint64, P]
+            lib.oracle_lookup.restype = None
+            lib.oracle_lookup.argtypes = [P, i64, i64, P, i64, P]
             lib.oracle_type_gradient.argtypes = [P, P, P, ctypes.c_int, i64,
                                                  ctypes.c_uint32, P, P]
             _lib = lib
@@ -290,6 +292,17 @@ def sync_unique_compressed(J_list, delta_list, E, lr, F):
     update_rows(E, Ihat, Mhat.astype(np.float64), lr)    # step 7
     return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M32=M32, Q=Q, S=S,
                 Qhat=Qhat, Mhat=Mhat, E=E)
+
+
+def lookup(E, J):
+    """Forward lookup: out[p] = E[J[p]] (zero row for J[p] >= V)."""
+    lib = _load()
+    E = _f32(E)
+    J = _u32(J)
+    V, D = E.shape
+    out = np.empty((J.size, D), np.float32)
+    lib.oracle_lookup(_p(E), V, D, _p(J), J.size, _p(out))
+    return out
 
 
 # ------------------------------------------------------------ seeding (3.2)

@@ -296,3 +296,15 @@ int64_t oracle_draw_samples(uint64_t seed, uint64_t step, int64_t S, uint64_t V,
   }
   return i;
 }
+
+/*
+ * Forward lookup ("A |V| x D embedding matrix projects the input K
+ * token sequence into a dense K x D matrix"): out[p,:] = E[J[p],:]; an id >=
+ * V (outside the matrix) gives a zero row.
+ */
+void oracle_lookup(const float* E, int64_t V, int64_t D, const uint32_t* J, int64_t K,
+                   float* out) {
+  for (int64_t p = 0; p < K; ++p)
+    for (int64_t d = 0; d < D; ++d)
+      out[p * D + d] = (int64_t)J[p] < V ? E[(int64_t)J[p] * D + d] : 0.0f;
+}

@@ -154,6 +154,9 @@ struct ScatterArgs {
 };
 // One cooperative launch: scatter, cut-run fixup, and (a.table) the world-1 S6.
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
+// forward lookup: out[p] = E[ids[p]] (zero row for an id >= vocab)
+cudaError_t launch_lookup(const float* table, int D, const uint32_t* ids, int64_t n,
+                          uint32_t vocab, float* out, int num_sms, cudaStream_t s);
 // seeding (Sec. 3.2, R16): the first S distinct draws of the (seed, step) stream
 constexpr int DRAW_MAX_S = 8192;
 cudaError_t launch_draw_samples(uint64_t seed, uint64_t step, int S, uint64_t V, uint32_t* out,

@@ -479,6 +479,20 @@ lmscale_status lmscale_draw_samples(lmscale_ctx* ctx, uint64_t seed, uint64_t st
   return LMSCALE_OK;
 }
 
+lmscale_status lmscale_lookup(lmscale_ctx* ctx, const uint32_t* ids, int64_t k,
+                              const float* table, float* out, void* stream) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (k < 0 || (k > 0 && (!ids || !table || !out)))
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "lookup: k=%lld or NULL pointer", (long long)k);
+  cudaSetDevice(ctx->cfg.device);
+  begin_call(ctx);
+  CK(launch_lookup(table, (int)ctx->cfg.dim, ids, k, (uint32_t)ctx->cfg.vocab, out,
+                   ctx->num_sms, S(stream)));
+  if (k > 0) LAUNCHED(1);
+  end_call(ctx);
+  return LMSCALE_OK;
+}
+
 lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return LMSCALE_ERR_INVALID_ARG;
   if (mode != ctx->tmode && ctx->gexec) {  // the captured graph carries the old events

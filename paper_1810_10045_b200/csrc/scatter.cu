@@ -781,3 +781,52 @@ cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* ou
   return cudaGetLastError();
 }
 }  // namespace lms
+
+namespace lms {
+// ------------------------------------------------ forward lookup
+// out[p, :] = E[ids[p], :] -- the input-embedding projection of the K tokens
+// (SURVEY 8(f) row 4).  Warp per row, grid-stride, 128-bit accesses when the
+// rows allow; an id >= vocab gives a zero row.
+template <typename T>
+__global__ void __launch_bounds__(256) k_lookup(const float* __restrict__ table, int D,
+                                                const uint32_t* __restrict__ ids, int64_t n,
+                                                uint32_t vocab, float* __restrict__ out) {
+  const int C = D / (int)(sizeof(T) / sizeof(float));
+  const int lane = threadIdx.x & 31;
+  const T* E = reinterpret_cast<const T*>(table);
+  T* O = reinterpret_cast<T*>(out);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += nw) {
+    const uint32_t w = __ldg(ids + p);
+    const T* src = E + (size_t)w * C;
+    T* dst = O + (size_t)p * C;
+    if (w < vocab) {
+      int c = lane;
+      for (; c + 96 < C; c += 128) {
+        const T a0 = __ldg(src + c), a1 = __ldg(src + c + 32), a2 = __ldg(src + c + 64),
+                a3 = __ldg(src + c + 96);
+        __stcs(dst + c, a0);
+        __stcs(dst + c + 32, a1);
+        __stcs(dst + c + 64, a2);
+        __stcs(dst + c + 96, a3);
+      }
+      for (; c < C; c += 32) __stcs(dst + c, __ldg(src + c));
+    } else {
+      for (int c = lane; c < C; c += 32) dst[c] = T{};
+    }
+  }
+}
+
+cudaError_t launch_lookup(const float* table, int D, const uint32_t* ids, int64_t n,
+                          uint32_t vocab, float* out, int num_sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 7) / 8;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)out % 16 == 0;
+  if (v4)
+    k_lookup<float4><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, n, vocab, out);
+  else
+    k_lookup<float><<<(unsigned)blocks, 256, 0, s>>>(table, D, ids, n, vocab, out);
+  return cudaGetLastError();
+}
+}  // namespace lms

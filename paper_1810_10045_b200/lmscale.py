@@ -87,6 +87,7 @@ _plan_seeds = _sig("lmscale_plan_seeds", _S, [ctypes.c_int32, ctypes.c_int32, ct
                                                 ctypes.POINTER(ctypes.c_int32)])
 _draw_samples = _sig("lmscale_draw_samples", _S, [_P, ctypes.c_uint64, ctypes.c_uint64, _i64, _P,
                                                   _P])
+_lookup = _sig("lmscale_lookup", _S, [_P, _P, _i64, _P, _P, _P])
 _set_compression = _sig("lmscale_set_compression", _S, [_P, ctypes.c_float])
 _compress = _sig("lmscale_compress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
 _decompress = _sig("lmscale_decompress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
@@ -101,7 +102,7 @@ EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_u
             "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
             "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing", "lmscale_alloc_table",
             "lmscale_set_compression", "lmscale_compress", "lmscale_decompress",
-            "lmscale_plan_seeds", "lmscale_draw_samples", "lmscale_get_stats",
+            "lmscale_plan_seeds", "lmscale_draw_samples", "lmscale_lookup", "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
 
 
@@ -366,6 +367,15 @@ class Context:
         self._check(_draw_samples(self._h, int(seed) & (2**64 - 1), int(step) & (2**64 - 1), int(S),
                                   _ptr(out), _stream(stream)), "lmscale_draw_samples")
         return out[:S]
+
+    def lookup(self, ids, table, out=None, stream=None) -> torch.Tensor:
+        """Forward lookup out[p] = table[ids[p]]."""
+        ids = self._ids(ids)
+        if out is None:
+            out = torch.empty(ids.numel(), self.dim, dtype=torch.float32, device=self.device)
+        self._check(_lookup(self._h, _ptr(ids), ids.numel(), _ptr(table), _ptr(out),
+                            _stream(stream)), "lmscale_lookup")
+        return out
 
     def stats(self) -> dict:
         s = StatsC()

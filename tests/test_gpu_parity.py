@@ -485,3 +485,21 @@ def test_draw_samples_rejects_bad_sizes(lm):
         with pytest.raises(lm.LmscaleError):
             ctx.draw_samples(1, 1, S)
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "1b"])
+@pytest.mark.parametrize("D_override", [None, 37])
+def test_lookup_bit_exact(lm, name, D_override):
+    """lmscale_lookup == oracle.lookup (row copies: bit-exact), 128-bit and
+    scalar paths, out-of-range ids -> zero rows."""
+    cfg = synth.CONFIGS[name]
+    D = D_override or cfg.D
+    V = cfg.V if D_override is None else 5000
+    J = synth.zipf_ids(V, 1.0, 3001)
+    J[[5, 17]] = [V, 2**32 - 1]
+    E = synth.table_values(V, D, "signed")
+    ctx = lm.Context(V, 16, D)
+    out = ctx.lookup(to_dev_ids(J), E.to(dev()))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.lookup(E.numpy(), J))
+    ctx.close()

@@ -242,3 +242,18 @@ def test_tolerance_metric_signed():
         for p in range(cfg.K):
             Ms[out["ranks"][g]["slot"][p]] += delta[g][p]
     check_rows(Ms, out["Mhat64"], A, "signed", "sequential fp32")
+
+
+def test_lookup_vs_numpy_and_special_cases():
+    """Forward lookup against numpy fancy indexing; identity ids
+    give E back; equal ids repeat one row; ids >= V give zero rows."""
+    rng = np.random.default_rng(4)
+    E = rng.standard_normal((97, 13)).astype(np.float32)
+    J = rng.integers(0, 97, 500).astype(np.uint32)
+    np.testing.assert_array_equal(oracle.lookup(E, J), E[J])
+    np.testing.assert_array_equal(oracle.lookup(E, np.arange(97, dtype=np.uint32)), E)
+    out = oracle.lookup(E, np.full(5, 3, np.uint32))
+    assert (out == E[3]).all()
+    out = oracle.lookup(E, np.array([1, 97, 2**32 - 1], np.uint32))
+    np.testing.assert_array_equal(out[0], E[1])
+    assert (out[1:] == 0).all()
