@@ -374,7 +374,7 @@ struct NvlsState {
 NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char* err,
                        size_t errlen) {
   NvlsState* st = new NvlsState();
-  st->ctas = num_sms < 128 ? num_sms : 128;
+  st->ctas = num_sms;  // one CTA per SM (measured: 128 -> 148 CTAs, 1b G=4 264 -> 260 us)
   if (const char* e = getenv("LMSCALE_NVLS_CTAS")) st->ctas = atoi(e);
   ncclResult_t r = ncclCommWindowRegister(comm, M, bytes, &st->win, NCCL_WIN_COLL_SYMMETRIC);
   if (r != ncclSuccess) {
