@@ -133,6 +133,7 @@ struct ScatterArgs {
   float* part2;           // level-2 partial rows, one per entry (fix_cap x D)
   int fix_cap;
   int fx_last;            // 1: last-arriver fix-up (no grid barrier); 0: listed fix-up phase
+  int fxp;                // last-arriver fix-up: partials per part
   uint32_t* fxcnt;        // last-arriver counters: parts [fx_stride], runs [fx_stride]
   int64_t fx_stride;      // nchunks x column blocks
   int zero_rows;          // 0: every slot is present locally (world 1): slot = local index

@@ -317,6 +317,8 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fix_cap = (int)(2 * ctx->nchunks);
   static const bool fx_barrier = getenv("LMSCALE_S4_FIXUP_BARRIER") != nullptr;
   a.fx_last = fx_barrier ? 0 : 1;
+  static const int fxp = getenv("LMSCALE_S4_FXP") ? atoi(getenv("LMSCALE_S4_FXP")) : 32;
+  a.fxp = fxp > 0 ? fxp : 32;
   a.fxcnt = ctx->fxcnt;
   a.fx_stride = ctx->fx_stride;
   a.zero_rows = ctx->cfg.world > 1 ? 1 : 0;  // world 1: slot = local index

@@ -131,7 +131,6 @@ __device__ __forceinline__ void emit_row(const ScatterArgs& a, size_t slot, uint
 // and the last part to finish sums the level-2 rows in part order.  Fixed
 // summation order: deterministic.  Counters reset themselves for the next
 // launch.
-constexpr int FXP = 32;
 
 // partial rows k in [k0, k0 + n) of the run starting at chunk c0, summed in k order
 template <typename T, int NV>
@@ -168,6 +167,7 @@ __device__ __forceinline__ void fix_arrive(const ScatterArgs& a, int u, int c0, 
   using V = Vec<T>;
   uint32_t* pcnt = a.fxcnt;
   uint32_t* rcnt = a.fxcnt + a.fx_stride;
+  const int FXP = a.fxp;  // partials per part
   const int j = k / FXP, nparts = (np + FXP - 1) / FXP;
   // ids of a part / a run = the partial-row index of its first piece (unique:
   // every partial row belongs to exactly one run): counter and level-2 row
@@ -199,13 +199,24 @@ __device__ __forceinline__ void fix_arrive(const ScatterArgs& a, int u, int c0, 
     const T* L2b = reinterpret_cast<const T*>(a.part2);
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-    for (int jj = 0; jj < nparts; ++jj)
+    for (int jj = 0; jj < nparts; jj += 2) {
+      T r2[2][NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v)
-        if (col0 + v * 32 < C)
-          acc[v] = V::add(acc[v], V::ld_l2(L2b + (size_t)(jj == 0 ? 2 * c0 + 1
-                                                                  : 2 * (c0 + jj * FXP)) * C +
-                                           col0 + v * 32));
+      for (int q = 0; q < 2; ++q) {
+        const int jq = jj + q;
+        const size_t row = jq == 0 ? (size_t)(2 * c0 + 1) : (size_t)(2 * (c0 + jq * FXP));
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          r2[q][v] = V::zero();
+          if (jq < nparts && col0 + v * 32 < C) r2[q][v] = V::ld_l2(L2b + row * C + col0 + v * 32);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (jj + q < nparts)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[v] = V::add(acc[v], r2[q][v]);
+    }
   }
   const int slot = a.zero_rows ? __ldcg(a.l2g + u) : u;
   if (slot < 0) return;
