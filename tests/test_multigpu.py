@@ -36,7 +36,12 @@ def _gloo_worker(rank, world, port, q):
     assert nid == fake
     m = D.max_over_ranks(10.0 + rank)
     b = D.broadcast_bytes(b"x" * (rank + 1) if rank == 1 else None, src=1)
-    q.put((rank, nid == fake, m, b))
+    # seed plan (Sec. 3.2): host logic every rank runs independently must agree
+    from paper_1810_10045_b200 import lmscale
+    plans = [None] * world
+    dist.all_gather_object(plans, lmscale.plan_seeds(8, "power", 0.64, master_seed=5))
+    same_plan = all(p == plans[0] for p in plans)
+    q.put((rank, nid == fake and same_plan, m, b))
     dist.barrier()
     dist.destroy_process_group()
 
