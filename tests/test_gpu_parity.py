@@ -503,3 +503,21 @@ def test_lookup_bit_exact(lm, name, D_override):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out.cpu().numpy(), oracle.lookup(E.numpy(), J))
     ctx.close()
+
+
+def test_toy_lm_dense_equals_unique_loss():
+    """a toy pooled-embedding LM trained through the
+    library -- forward lookup, exchange, update -- has per-step losses that
+    agree between the uniqueness exchange and the dense baseline (P:769-771:
+    the method reaches the dense result), and the loss goes down."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "toy_lm", os.path.join(os.path.dirname(os.path.dirname(__file__)), "examples", "toy_lm.py"))
+    toy = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(toy)
+    u = toy.run(8, "unique")
+    d = toy.run(8, "dense")
+    for a, b in zip(u, d):
+        assert abs(a - b) <= 1e-5 * abs(b), (u, d)
+    assert u[-1] < u[0]
