@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
     prev = skv[li0 - 1].x;
   else if (cr > 0)
     prev = cl.map_shared_rank(skv, cr - 1)[CL_TILE - 1].x;
+  const uint32_t prev_first = prev;  // key before this thread's slice (word heads)
   uint32_t sk[IT];
   int32_t sv[IT];
 #pragma unroll
@@ -241,10 +242,14 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
           a.ihat[u_run] = key;
           a.l2g[u_run] = (int32_t)u_run;
         }
-        if (key < a.vocab)
+        if (key < a.vocab) {
           atomicOr(a.lbits + (key >> 5), 1u << (key & 31u));
-        else
+          // first present id of its 32-id word: the word's local base index
+          const uint32_t pkey = j == 0 ? prev_first : sk[j > 0 ? j - 1 : 0];
+          if (a.lrank && (gi == 0 || (pkey >> 5) != (key >> 5))) a.lrank[key >> 5] = u_run;
+        } else {
           bad2 = true;
+        }
         ++u_run;
       }
       a.segidx[gi] = (int32_t)u_run - 1;

@@ -251,9 +251,11 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
   uint32_t heads = 0;
   uint32_t sk[IT];
   int32_t sv[IT];
+  uint32_t prev_first = 0;  // key before this thread's slice (word heads)
   auto load_sorted = [&](int t) {
     const int i0 = t * CO_TILE + tid * IT;
     uint32_t prev = (i0 > 0 && i0 <= K) ? __ldcg(kin + i0 - 1) : 0u;
+    prev_first = prev;
     heads = 0;
 #pragma unroll
     for (int j = 0; j < IT; ++j) {
@@ -293,10 +295,13 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s1(S1Args a) {
             a.ihat[u_run] = sk[j];
             a.l2g[u_run] = (int32_t)u_run;
           }
-          if (sk[j] < a.vocab)
+          if (sk[j] < a.vocab) {
             atomicOr(a.lbits + (sk[j] >> 5), 1u << (sk[j] & 31u));
-          else
+            const uint32_t pkey = j == 0 ? prev_first : sk[j > 0 ? j - 1 : 0];
+            if (a.lrank && (i == 0 || (pkey >> 5) != (sk[j] >> 5))) a.lrank[sk[j] >> 5] = u_run;
+          } else {
             bad2 = true;
+          }
           ++u_run;
         }
         a.segidx[i] = (int32_t)u_run - 1;

@@ -60,6 +60,7 @@ struct S1Args {
   int32_t* segidx;
   int32_t* inverse;
   uint32_t* lbits;
+  uint32_t* lrank;  // optional: lrank[w] = local index of the first present id of word w
   int64_t W;
   uint32_t* heads;  // [ntiles]
   Sc1* sc;
@@ -187,7 +188,8 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st);
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
-                        float cF, size_t mhat_off, cudaStream_t s);
+                        float cF, size_t mhat_off, size_t lrank_off, int local_m,
+                        cudaStream_t s);
 // true: the peer-to-peer fused kernel (presence-aware) is used for this G
 bool nvls_use_p2p(int world);
 // LSA base of every rank's M window (world entries written to out_host)

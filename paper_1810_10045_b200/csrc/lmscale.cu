@@ -53,6 +53,7 @@ struct lmscale_ctx {
   SortPlan plan{}, cl_plan{};
   cudaStream_t s_side = nullptr, s_copy = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_s1 = nullptr, ev_s3 = nullptr, ev_copy = nullptr;
+  cudaEvent_t ev_s4 = nullptr;
   cudaEvent_t tev[EV_COUNT] = {};
   bool timing_valid = false, update_timed = false;
   ncclComm_t comm = nullptr;
@@ -73,6 +74,8 @@ struct lmscale_ctx {
   size_t lbits_off = 0;        // byte offset of lbits inside the M window
   size_t mhat_off = 0;         // byte offset of the compressed M^ rows inside the M window
   size_t flags_off = 0;        // byte offset of the S3 handshake flags inside the M window
+  size_t lrank_off = 0;        // byte offset of lrank (per-word local base index) in the window
+  uint32_t* lrank = nullptr;   // S1 output for the local-slot M layout (window only)
   char* peer_base[8] = {};     // LSA base of every rank's M window
   bool peer_s3 = false;        // S3 ORs the peers' local bitmaps (no ID all-gather)
   uint32_t* s3_epoch = nullptr;
@@ -214,6 +217,7 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   a.segidx = ctx->segidx;
   a.inverse = ctx->inverse;
   a.lbits = ctx->lbits;
+  a.lrank = ctx->lrank;
   a.W = ctx->W;
   a.heads = ctx->heads;
   a.sc = ctx->sc1;
@@ -341,8 +345,9 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
 // S4 (+ the world-1 S6 when table != nullptr): one cooperative launch.
 lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
                       float* table = nullptr, float lr = 0.f, bool fill_absent = true,
-                      float m16_F = 0.f, bool apply = false) {
+                      float m16_F = 0.f, bool apply = false, bool local_slots = false) {
   ScatterArgs a = scatter_args(ctx, grad);
+  if (local_slots) a.zero_rows = 0;  // row u of M for the u-th local word
   a.table = table;
   a.lr = lr;
   a.apply = apply ? 1 : 0;
@@ -608,6 +613,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_s3, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_s4, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&ctx->s_cap, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
@@ -621,7 +627,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       // M and this rank's local presence bitmap share one symmetric window:
       // the fused kernel reads the peers' bitmaps to load only present rows
       const size_t lb_off = m_bytes;
-      const size_t fl_off = align_up(m_bytes + 4 * (size_t)ctx->W, 256);
+      const size_t lr_off = align_up(m_bytes + 4 * (size_t)ctx->W, 256);
+      const size_t fl_off = align_up(lr_off + 4 * (size_t)ctx->W, 256);
       const size_t win_bytes = align_up(fl_off + 4 * 64, 1 << 21);
       void* m = nullptr;
       if (ncclMemAlloc(&m, win_bytes) != ncclSuccess)
@@ -639,6 +646,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
         ctx->lbits = (uint32_t*)((char*)m + lb_off);
         ctx->lbits_off = lb_off;
         ctx->flags_off = fl_off;
+        ctx->lrank_off = lr_off;
+        ctx->lrank = (uint32_t*)((char*)m + lr_off);
         ctx->peer_s3 = !getenv("LMSCALE_NO_PEER_S3") && cfg->world <= 8 &&
                        nvls_peer_bases(ctx->nvls, cfg->world, (void**)ctx->peer_base);
       } else {
@@ -697,6 +706,7 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
   if (ctx->ev_s3) cudaEventDestroy(ctx->ev_s3);
+  if (ctx->ev_s4) cudaEventDestroy(ctx->ev_s4);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   if (ctx->s_side) cudaStreamDestroy(ctx->s_side);
   if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
@@ -829,6 +839,19 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   const uint32_t* I = ids;
   int64_t n = k;
   const bool peer_s3 = G > 1 && ctx->peer_s3;
+  // compressed exchange (R15): S4 writes binary16 rows, present rows only
+  const bool comp = G > 1 && ctx->cF > 0.f;
+  // the peer-to-peer fused kernels load only present rows: no zero-fill of M
+  const bool p2p = G > 1 && table && ctx->nvls &&
+                   (comp || (table == ctx->table_ptr && ctx->table_win && nvls_use_p2p(G)));
+  // local-slot layout (small K, peer S3, P2P): S4 writes row u of M_g for the
+  // u-th local word (no l2g needed), so it runs on the side stream while S3
+  // runs -- safe because this S4 variant has no grid barrier.  The fused
+  // kernel finds word w's row on rank j as lrank_j[w/32] + popc(bits below w).
+  static const bool no_local = getenv("LMSCALE_NO_S4_OVERLAP") != nullptr;
+  static const bool fx_barrier = getenv("LMSCALE_S4_FIXUP_BARRIER") != nullptr;
+  const bool local_m = peer_s3 && p2p && ctx->lrank && k < (1 << 16) && !fx_barrier && !no_local;
+  const bool overlap = local_m && ctx->tmode == 0;  // timed passes measure S4 alone
   if (peer_s3) {
     // J^-set exchange: no ID all-gather; S3 ORs the G
     // local presence bitmaps over NVLink after S1 (same I^, U_g and l2g).
@@ -837,6 +860,13 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     if (st) return st;
     rec(ctx, EV_S1_END, s);
     rec(ctx, EV_GATHER_END, s);
+    if (overlap) {
+      CK(cudaEventRecord(ctx->ev_s1, s));
+      CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_s1, 0));
+      st = run_s4(ctx, grad, ctx->s_side, nullptr, lr, false, comp ? ctx->cF : 0.f, false, true);
+      if (st) return st;
+      CK(cudaEventRecord(ctx->ev_s4, ctx->s_side));
+    }
   } else if (G > 1) {
     // S1 on the side stream, concurrent with the S2 ID all-gather.
     CK(cudaEventRecord(ctx->ev_fork, s));
@@ -881,25 +911,24 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   // (fusing S6 into S4's cooperative kernel at world 1 was measured slower
   // than the separate, higher-occupancy update launch; kept separate)
   const bool fuse_s6 = false;
-  // the peer-to-peer fused kernel loads only present rows: no zero-fill of M
-  // compressed exchange (R15): S4 writes binary16 rows, present rows only
-  const bool comp = G > 1 && ctx->cF > 0.f;
-  const bool p2p = G > 1 && table && ctx->nvls &&
-                   (comp || (table == ctx->table_ptr && ctx->table_win && nvls_use_p2p(G)));
   // world 1: S6 folded into S4 (finished rows go straight into the table; M
   // is not written and not re-read).  LMSCALE_NO_INLINE_S6: separate k_update.
   static const bool no_inline = getenv("LMSCALE_NO_INLINE_S6") != nullptr;
   const bool inline_s6 = G == 1 && table && !no_inline;
-  st = run_s4(ctx, grad, s, (fuse_s6 || inline_s6) ? table : nullptr, lr,
-              /*fill_absent=*/G > 1 && !p2p, comp ? ctx->cF : 0.f, inline_s6);
-  if (st) return st;
+  if (overlap) {
+    CK(cudaStreamWaitEvent(s, ctx->ev_s4, 0));  // S4 ran beside S3
+  } else {
+    st = run_s4(ctx, grad, s, (fuse_s6 || inline_s6) ? table : nullptr, lr,
+                /*fill_absent=*/G > 1 && !p2p, comp ? ctx->cF : 0.f, inline_s6, local_m);
+    if (st) return st;
+  }
   rec(ctx, EV_FIXUP_END, s);
   if (G > 1 && table && ctx->nvls) {
     // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
                        ctx->cfg.rank, G, ctx->trace,
                        table == ctx->table_ptr ? ctx->table_win : nullptr, ctx->lbits_off,
-                       comp ? ctx->cF : 0.f, ctx->mhat_off, s);
+                       comp ? ctx->cF : 0.f, ctx->mhat_off, ctx->lrank_off, local_m ? 1 : 0, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {

@@ -87,6 +87,8 @@ struct NvlsKernelArgs {
                       // multicast straight into every replica of E (no copy phase)
   float cF;           // compression scale F (k_p2p_update_c)
   size_t mhat_off;    // byte offset of the compressed M^ rows in the M window
+  size_t lrank_off;   // local-slot layout: byte offset of lrank in the window
+  int local_m;        // 1: M_j rows are at rank j's local index (lrank + popcount), else at r
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -214,12 +216,14 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
     pe[j] = j < a.world ? reinterpret_cast<T*>(ncclGetLsaPointer(a.twin, 0, j)) : nullptr;
   }
   const uint32_t* pb[MAXG];  // each rank's local presence bitmap (S1's lbits)
+  const uint32_t* pr[MAXG];  // each rank's lrank (local-slot layout)
 #pragma unroll
-  for (int j = 0; j < MAXG; ++j)
-    pb[j] = j < a.world ? reinterpret_cast<const uint32_t*>(
-                              reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j)) +
-                              a.lbits_off)
-                        : nullptr;
+  for (int j = 0; j < MAXG; ++j) {
+    const char* base =
+        j < a.world ? reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    pb[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
+    pr[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
+  }
   const T* E = reinterpret_cast<const T*>(a.table);
   for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
     const int64_t r = a.rank + a.world * t;
@@ -229,9 +233,17 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
     // which ranks hold word w: only their copies of M[r] are loaded (absent
     // ranks' rows are never written: S4 skips the zero-fill on this path)
     uint32_t has = 0;
+    size_t lrow[MAXG];  // row of word w in rank j's M
 #pragma unroll
-    for (int j = 0; j < MAXG; ++j)
-      if (j < a.world) has |= ((__ldcg(pb[j] + (w >> 5)) >> (w & 31u)) & 1u) << j;
+    for (int j = 0; j < MAXG; ++j) {
+      lrow[j] = mrow;
+      if (j < a.world) {
+        const uint32_t bits = __ldcg(pb[j] + (w >> 5));
+        has |= ((bits >> (w & 31u)) & 1u) << j;
+        if (a.local_m)
+          lrow[j] = (size_t)(__ldcg(pr[j] + (w >> 5)) + __popc(bits & ((1u << (w & 31u)) - 1u))) * C;
+      }
+    }
     for (int c = lane; c < C; c += 128) {
       T m[4], e[4];
 #pragma unroll
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
           T v[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            v[q] = (c + 32 * q < C) ? __ldcg(pm[j] + mrow + c + 32 * q) : T{};
+            v[q] = (c + 32 * q < C) ? __ldcg(pm[j] + lrow[j] + c + 32 * q) : T{};
 #pragma unroll
           for (int q = 0; q < 4; ++q) m[q] = add4(m[q], v[q]);  // rank order
         }
@@ -294,21 +306,31 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
   const H* pm[MAXG];
   H* pq[MAXG];
   const uint32_t* pb[MAXG];
+  const uint32_t* pr[MAXG];
 #pragma unroll
   for (int j = 0; j < MAXG; ++j) {
     char* base = j < a.world ? reinterpret_cast<char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
     pm[j] = reinterpret_cast<const H*>(base);
     pq[j] = reinterpret_cast<H*>(base + a.mhat_off);
     pb[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
+    pr[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
   }
   for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
     const int64_t r = a.rank + a.world * t;
     const uint32_t w = __ldg(a.ihat + r);
     const size_t mrow = (size_t)r * C;
     uint32_t has = 0;
+    size_t lrow[MAXG];  // row of word w in rank j's M
 #pragma unroll
-    for (int j = 0; j < MAXG; ++j)
-      if (j < a.world) has |= ((__ldcg(pb[j] + (w >> 5)) >> (w & 31u)) & 1u) << j;
+    for (int j = 0; j < MAXG; ++j) {
+      lrow[j] = mrow;
+      if (j < a.world) {
+        const uint32_t bits = __ldcg(pb[j] + (w >> 5));
+        has |= ((bits >> (w & 31u)) & 1u) << j;
+        if (a.local_m)
+          lrow[j] = (size_t)(__ldcg(pr[j] + (w >> 5)) + __popc(bits & ((1u << (w & 31u)) - 1u))) * C;
+      }
+    }
     for (int c = lane; c < C; c += 128) {
       T m[4];
 #pragma unroll
@@ -319,7 +341,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
           H v[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (c + 32 * q < C) v[q] = pm[j][mrow + c + 32 * q];
+            if (c + 32 * q < C) v[q] = pm[j][lrow[j] + c + 32 * q];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (c + 32 * q < C) m[q] = add4(m[q], dech(v[q], F));  // rank order, fp32
@@ -450,8 +472,11 @@ void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w) {
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
-                        float cF, size_t mhat_off, cudaStream_t s) {
+                        float cF, size_t mhat_off, size_t lrank_off, int local_m,
+                        cudaStream_t s) {
   NvlsKernelArgs a;
+  a.lrank_off = lrank_off;
+  a.local_m = local_m;
   a.lbits_off = lbits_off;
   a.cF = cF;
   a.mhat_off = mhat_off;
