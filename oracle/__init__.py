@@ -78,6 +78,10 @@ def _load():
             lib.oracle_compress.argtypes = [P, i64, ctypes.c_float, P]
             lib.oracle_decompress.restype = None
             lib.oracle_decompress.argtypes = [P, i64, ctypes.c_float, P]
+            lib.oracle_compress_bf16.restype = None
+            lib.oracle_compress_bf16.argtypes = [P, i64, ctypes.c_float, P]
+            lib.oracle_decompress_bf16.restype = None
+            lib.oracle_decompress_bf16.argtypes = [P, i64, ctypes.c_float, P]
             lib.oracle_sum_f32.restype = None
             lib.oracle_sum_f32.argtypes = [P, ctypes.c_int, i64, P]
             lib.oracle_mix64.restype = ctypes.c_uint64
@@ -229,22 +233,25 @@ def sync_unique(J_list, delta_list, E, lr):
                 Mhat64=Mhat64, Mhat=Mhat64.astype(np.float32), E=E)
 
 
-def compress(x, F):
-    """Sec. 3.3: binary16 bits (uint16) of RNE(fp32(F * x)),
-    saturated to +-65504 (R15)."""
+def compress(x, F, fmt="fp16"):
+    """Sec. 3.3: 16-bit payload (uint16 bits) of RNE(fp32(F * x)),
+    saturated to the format's largest finite value (DESIGN.md R15);
+    fmt = "fp16" (binary16, the paper's) or "bf16"."""
     lib = _load()
     x = _f32(x)
     q = np.empty(x.shape, np.uint16)
-    lib.oracle_compress(_p(x), x.size, float(F), _p(q))
+    fn = lib.oracle_compress if fmt == "fp16" else lib.oracle_compress_bf16
+    fn(_p(x), x.size, float(F), _p(q))
     return q
 
 
-def decompress(q, F):
-    """Sec. 3.3 (P:511): fp32(half) / F."""
+def decompress(q, F, fmt="fp16"):
+    """Sec. 3.3 (P:511): fp32(payload) / F."""
     lib = _load()
     q = np.ascontiguousarray(q, dtype=np.uint16)
     x = np.empty(q.shape, np.float32)
-    lib.oracle_decompress(_p(q), q.size, float(F), _p(x))
+    fn = lib.oracle_decompress if fmt == "fp16" else lib.oracle_decompress_bf16
+    fn(_p(q), q.size, float(F), _p(x))
     return x
 
 
@@ -257,7 +264,7 @@ def sum_f32(a_list):
     return out
 
 
-def sync_unique_compressed(J_list, delta_list, E, lr, F):
+def sync_unique_compressed(J_list, delta_list, E, lr, F, fmt="fp16"):
     """The uniqueness exchange with compression (Sec. 3.3 on Sec. 3.1).
 
     Steps 1-5 as ``sync_unique``; each M_i is an FP32 tensor, so it is
@@ -285,10 +292,10 @@ def sync_unique_compressed(J_list, delta_list, E, lr, F):
         r["l2g"], r["slot"] = remap(r["Jhat"], Ihat, r["inverse"])
         m = scatter_expand(r["dhat"], r["l2g"], Ug).astype(np.float32)   # step 5
         M32.append(m)
-        Q.append(compress(m, F))                         # 6a: down-cast on the sender
-    S = sum_f32([decompress(q, F) for q in Q])           # 6a: up-cast, sum (receiver)
-    Qhat = compress(S, F)                                # 6b: the reduced rows, down-cast
-    Mhat = decompress(Qhat, F)                           # 6b: up-cast on every rank
+        Q.append(compress(m, F, fmt))                    # 6a: down-cast on the sender
+    S = sum_f32([decompress(q, F, fmt) for q in Q])      # 6a: up-cast, sum (receiver)
+    Qhat = compress(S, F, fmt)                           # 6b: the reduced rows, down-cast
+    Mhat = decompress(Qhat, F, fmt)                      # 6b: up-cast on every rank
     update_rows(E, Ihat, Mhat.astype(np.float64), lr)    # step 7
     return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M32=M32, Q=Q, S=S,
                 Qhat=Qhat, Mhat=Mhat, E=E)

@@ -308,3 +308,32 @@ void oracle_lookup(const float* E, int64_t V, int64_t D, const uint32_t* J, int6
     for (int64_t d = 0; d < D; ++d)
       out[p * D + d] = (int64_t)J[p] < V ? E[(int64_t)J[p] * D + d] : 0.0f;
 }
+
+/*
+ * bfloat16 variant of the codec ("fp16 (and bf16)";
+ * reading R15): down-cast = round-to-nearest-even of fp32(F * x) to the upper
+ * 16 bits (8-bit exponent, 7-bit mantissa), saturating to +-(largest finite
+ * bfloat16) = +-0x7F7F; up-cast = the 16 bits as the top of an fp32, then one
+ * fp32 division by F.  Inputs are finite.
+ */
+void oracle_compress_bf16(const float* x, int64_t n, float F, uint16_t* q) {
+  const float maxbf = 3.3895313892515355e38f; /* bits 0x7F7F0000 */
+  for (int64_t i = 0; i < n; ++i) {
+    float p = F * x[i];
+    if (p > maxbf) p = maxbf;
+    if (p < -maxbf) p = -maxbf;
+    uint32_t u;
+    memcpy(&u, &p, sizeof(u));
+    uint32_t r = u + 0x7FFFu + ((u >> 16) & 1u); /* ties to even on the dropped half */
+    q[i] = (uint16_t)(r >> 16);
+  }
+}
+
+void oracle_decompress_bf16(const uint16_t* q, int64_t n, float F, float* x) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u = (uint32_t)q[i] << 16;
+    float v;
+    memcpy(&v, &u, sizeof(v));
+    x[i] = v / F;
+  }
+}

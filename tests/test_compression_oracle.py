@@ -165,3 +165,73 @@ def test_exchange_saturates():
     # col 0: 100 -> 102400 saturates to 65504 on each rank, sum 131008 -> 65504
     # col 1: 65504 - 65504 = 0; col 2: 65504 + 0
     np.testing.assert_array_equal(got["Mhat"][0], np.float32([65504, 0, 65504]) / 1024)
+
+
+# ------------------------------------------------------------ bfloat16 variant
+
+def _torch_bf16(x, F):
+    """torch's float32 -> bfloat16 (round to nearest even) of fp32(F * x),
+    saturated to the largest finite bfloat16 (R15)."""
+    import torch
+    p = (np.float32(F) * np.asarray(x, np.float32)).astype(np.float32)
+    m = np.float32(3.3895313892515355e38)
+    p = np.clip(p, -m, m)
+    return torch.from_numpy(p).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+
+
+def test_bf16_golden_values():
+    """Hand-written bfloat16 encodings: 1.0 = 0x3F80; 1 + 2^-8 is a tie -> even
+    0x3F80; 1 + 3*2^-8 is a tie between 1 + 2^-7 and 1 + 2^-6 -> even 0x3F82
+    (= 1 + 2^-6); -2 = 0xC000; saturation to 0x7F7F / 0xFF7F."""
+    x = np.float32([1.0, 1 + 2**-8, 1 + 3 * 2**-8, -2.0, 3.4e38, -3.4e38, 0.0])
+    want = [0x3F80, 0x3F80, 0x3F82, 0xC000, 0x7F7F, 0xFF7F, 0x0000]
+    assert oracle.compress(x, 1.0, "bf16").tolist() == want
+    back = oracle.decompress(np.uint16(want), 1.0, "bf16")
+    assert back[0] == 1.0 and back[2] == np.float32(1 + 2**-6) and back[3] == -2.0
+
+
+@pytest.mark.parametrize("F", [1.0, 3.0, 1024.0])
+def test_bf16_matches_torch_rne(F):
+    rng = np.random.default_rng(int(F) + 11)
+    x = np.concatenate([
+        rng.standard_normal(50000).astype(np.float32),
+        (rng.standard_normal(20000) * 1e-38).astype(np.float32),     # subnormal range
+        (rng.standard_normal(5000) * 1e36).astype(np.float32),
+        rng.integers(-70000, 70000, 20000).astype(np.float32),       # ties
+    ])
+    np.testing.assert_array_equal(oracle.compress(x, F, "bf16"), _torch_bf16(x, F))
+
+
+def test_bf16_round_trip_and_error():
+    bits = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    vals = (bits.astype(np.uint32) << 16).view(np.float32)
+    finite = np.isfinite(vals)
+    np.testing.assert_array_equal(oracle.compress(vals[finite], 1.0, "bf16"), bits[finite])
+    np.testing.assert_array_equal(oracle.decompress(bits[finite], 1.0, "bf16"), vals[finite])
+    rng = np.random.default_rng(5)
+    x = (np.exp2(rng.uniform(-100, 100, 100000)) * rng.choice([-1, 1], 100000)).astype(np.float32)
+    back = oracle.decompress(oracle.compress(x, 1.0, "bf16"), 1.0, "bf16").astype(np.float64)
+    assert (np.abs(back - x) / np.abs(x)).max() <= 2.0 ** -8
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_bf16_exchange_exact_case_and_bound(G):
+    """Integers <= 256 are exact in bfloat16: the bf16 exchange equals the
+    plain one; in SIGNED mode it stays within 2^-7 (sum|M_g| + |M^|)."""
+    rng = np.random.default_rng(G)
+    J = [rng.integers(0, 40, 16).astype(np.uint32) for _ in range(G)]
+    Dl = [rng.integers(-4, 4, (16, 4)).astype(np.float32) for _ in range(G)]
+    E0 = (rng.integers(-16, 16, (40, 4)) / 16).astype(np.float32)
+    ref = oracle.sync_unique(J, Dl, E0.copy(), 2.0 ** -4)
+    assert np.abs(ref["Mhat64"]).max() <= 256
+    got = oracle.sync_unique_compressed(J, Dl, E0.copy(), 2.0 ** -4, 1.0, "bf16")
+    np.testing.assert_array_equal(got["Mhat"], ref["Mhat64"].astype(np.float32))
+    cfg = synth.CONFIGS["tiny"].with_(G=G)
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    Dl = [synth.grad_values(cfg.K, cfg.D, "signed", rank=g).numpy() for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, "signed").numpy()
+    ref = oracle.sync_unique(J, Dl, E0.copy(), 0.1)
+    got = oracle.sync_unique_compressed(J, Dl, E0.copy(), 0.1, 1.0, "bf16")
+    absM = sum(np.abs(m) for m in ref["M"])
+    bound = 2.0 ** -7 * (absM + np.abs(ref["Mhat64"])) + 1e-37
+    assert (np.abs(got["Mhat"].astype(np.float64) - ref["Mhat64"]) <= bound).all()
