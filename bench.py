@@ -49,6 +49,8 @@ def parse():
                          "candidates per GPU with its seed group's seed, then exchanges "
                          "[K targets || samples]")
     ap.add_argument("--samples", type=int, default=1024, help="sampled-softmax S per GPU (P:605)")
+    ap.add_argument("--codec", default="fp16", choices=["fp16", "bf16"],
+                    help="16-bit payload format of --compress")
     ap.add_argument("--compress", type=float, default=0.0,
                     help="Sec. 3.3 compressed exchange with scale F (0 = off, fp32 rows)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -187,7 +189,8 @@ def config_dict(cfg, args, world):
             "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read sweep), "
                   "outside the timed region",
             "cuda_graph": not getattr(args, "no_graph", True),
-            "compression": f"fp16:F={args.compress:g}" if args.compress > 0 else "off",
+            "compression": (f"{getattr(args, 'codec', 'fp16')}:F={args.compress:g}"
+                            if args.compress > 0 else "off"),
             "seeding": (f"{args.seeding} (alpha 0.64), S={args.samples} samples/GPU; ids per "
                         f"GPU = K targets + S samples" if getattr(args, "seeding", None)
                         else "off (input-embedding exchange)")}
@@ -270,6 +273,7 @@ def main():
         table = synth.table_values(cfg.V, cfg.D, args.mode, device=dev)
     if args.compress > 0:
         ctx.set_compression(args.compress)
+        ctx.set_codec(args.codec)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 

@@ -272,8 +272,18 @@ LMSCALE_API lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode);
  * UNSUPPORTED. */
 LMSCALE_API lmscale_status lmscale_set_compression(lmscale_ctx* ctx, float F);
 
-/* The codec alone, device pointers, stream-ordered, i < n:
- * compress:   q[i] = binary16 bits of RNE(fp32(F * x[i])), saturated to +-65504;
+/* The 16-bit format of the compressed exchange and of lmscale_compress /
+ * lmscale_decompress ("fp16 (and bf16)"; R15):
+ * LMSCALE_CODEC_FP16 (binary16, the paper's, default; saturates at +-65504)
+ * or LMSCALE_CODEC_BF16 (bfloat16: same RNE of fp32(F * x), saturates at
+ * +-0x7F7F = +-3.3895e38).  INVALID_ARG for any other value. */
+#define LMSCALE_CODEC_FP16 0
+#define LMSCALE_CODEC_BF16 1
+LMSCALE_API lmscale_status lmscale_set_codec(lmscale_ctx* ctx, int32_t codec);
+
+/* The codec alone, device pointers, stream-ordered, i < n, in the
+ * context's 16-bit format (lmscale_set_codec; binary16 by default):
+ * compress:   q[i] = bits of RNE(fp32(F * x[i])), saturated (binary16: +-65504);
  * decompress: x[i] = fp32(q[i]) / F (exact widening, one fp32 division).
  * F > 0 and finite, n >= 0 (n == 0 launches nothing), else INVALID_ARG. */
 LMSCALE_API lmscale_status lmscale_compress(lmscale_ctx* ctx, const float* x, int64_t n, float F,

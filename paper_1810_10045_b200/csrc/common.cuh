@@ -1,6 +1,7 @@
 // common.cuh -- device helpers shared by the lmscale kernels (sm_100a).
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -155,26 +156,29 @@ inline void max_carveout(const void* f) {
 }
 
 // ---- compression codec (Sec. 3.3; R15) -------------
-// down-cast: binary16 round-to-nearest-even of the fp32 product F * x,
-// saturated to +-65504; up-cast: exact widening, then one fp32 division by F.
-__device__ __forceinline__ __half enc1(float x, float F) {
-  return __float2half_rn(fminf(fmaxf(__fmul_rn(F, x), -65504.f), 65504.f));
+// down-cast: round-to-nearest-even of the fp32 product F * x to a 16-bit
+// format, saturated to its largest finite value; up-cast: exact widening, then
+// one fp32 division by F.  bf == 0: binary16 (the paper's FP16); bf == 1:
+// bfloat16.  Payloads travel as raw 16-bit patterns.
+__device__ __forceinline__ uint16_t enc1(float x, float F, int bf) {
+  const float p = __fmul_rn(F, x);
+  if (bf) {
+    const float m = 3.3895313892515355e38f;  // largest finite bfloat16
+    return __bfloat16_as_ushort(__float2bfloat16_rn(fminf(fmaxf(p, -m), m)));
+  }
+  return __half_as_ushort(__float2half_rn(fminf(fmaxf(p, -65504.f), 65504.f)));
 }
-__device__ __forceinline__ uint32_t enc2(float x, float y, float F) {
-  const __half2 h = __halves2half2(enc1(x, F), enc1(y, F));
-  return *reinterpret_cast<const uint32_t*>(&h);
+__device__ __forceinline__ float dec1(uint16_t u, float F, int bf) {
+  const float v = bf ? __bfloat162float(__ushort_as_bfloat16(u)) : __half2float(__ushort_as_half(u));
+  return __fdiv_rn(v, F);
 }
-__device__ __forceinline__ float dec1(__half h, float F) { return __fdiv_rn(__half2float(h), F); }
-__device__ __forceinline__ float2 dec2(uint32_t u, float F) {
-  const __half2 h = *reinterpret_cast<const __half2*>(&u);
-  return make_float2(dec1(__low2half(h), F), dec1(__high2half(h), F));
+__device__ __forceinline__ uint2 enc4(float4 v, float F, int bf) {
+  return make_uint2((uint32_t)enc1(v.x, F, bf) | ((uint32_t)enc1(v.y, F, bf) << 16),
+                    (uint32_t)enc1(v.z, F, bf) | ((uint32_t)enc1(v.w, F, bf) << 16));
 }
-__device__ __forceinline__ uint2 enc4(float4 v, float F) {
-  return make_uint2(enc2(v.x, v.y, F), enc2(v.z, v.w, F));
-}
-__device__ __forceinline__ float4 dec4(uint2 u, float F) {
-  const float2 a = dec2(u.x, F), b = dec2(u.y, F);
-  return make_float4(a.x, a.y, b.x, b.y);
+__device__ __forceinline__ float4 dec4(uint2 u, float F, int bf) {
+  return make_float4(dec1((uint16_t)(u.x & 0xffffu), F, bf), dec1((uint16_t)(u.x >> 16), F, bf),
+                     dec1((uint16_t)(u.y & 0xffffu), F, bf), dec1((uint16_t)(u.y >> 16), F, bf));
 }
 
 }  // namespace lms

@@ -142,6 +142,7 @@ struct ScatterArgs {
   int m16;                // M rows are stored compressed (binary16 of cF * x, R15)
   int apply;              // world 1: S6 folded in -- finished rows update `table`, no M
   float cF;               // compression scale F
+  int cbf;                // codec: 0 binary16, 1 bfloat16
   int short_runs;         // finish runs <= FX_SHORT in their starting chunk (large K)
   float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
   float lr;
@@ -166,8 +167,8 @@ cudaError_t launch_draw_samples(uint64_t seed, uint64_t step, int S, uint64_t V,
 // seed-group plan; returns the number of groups, -1 on a bad policy / alpha
 int plan_seed_groups(int world, int policy, double alpha, uint64_t master, uint64_t* seeds);
 // compression codec (R15): down = compress (fp32 -> binary16 bits), else decompress
-cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* out, int num_sms,
-                         cudaStream_t s);
+cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, int bf, void* out,
+                         int num_sms, cudaStream_t s);
 
 // ---- S6 / S0 --------------------------------------------------------------
 // n_dev != nullptr: the row count is read on the device (min(n, *n_dev)); n
@@ -188,7 +189,7 @@ void nvls_destroy(ncclComm_t comm, NvlsState* st);
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
-                        float cF, size_t mhat_off, size_t lrank_off, int local_m,
+                        float cF, int cbf, size_t mhat_off, size_t lrank_off, int local_m,
                         cudaStream_t s);
 // true: the peer-to-peer fused kernel (presence-aware) is used for this G
 bool nvls_use_p2p(int world);

@@ -80,6 +80,7 @@ struct lmscale_ctx {
   bool peer_s3 = false;        // S3 ORs the peers' local bitmaps (no ID all-gather)
   uint32_t* s3_epoch = nullptr;
   float cF = 0.f;              // compression scale (0: off), lmscale_set_compression
+  int cbf = 0;                 // codec: 0 binary16, 1 bfloat16 (lmscale_set_codec)
   GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
   float* table_ptr = nullptr;  // lmscale_alloc_table
   size_t table_bytes = 0;
@@ -329,6 +330,7 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fill_absent = 1;
   a.m16 = 0;
   a.cF = 0.f;
+  a.cbf = 0;
   a.apply = 0;
   a.short_runs = ctx->last_k >= (1 << 16) ? 1 : 0;
   a.table = nullptr;
@@ -354,6 +356,7 @@ lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
   a.fill_absent = fill_absent ? 1 : 0;
   a.m16 = m16_F > 0.f ? 1 : 0;
   a.cF = m16_F;
+  a.cbf = ctx->cbf;
   CK(launch_scatter(a, s));
   LAUNCHED(1);
   rec(ctx, EV_SCATTER_END, s);
@@ -424,6 +427,18 @@ lmscale_status lmscale_alloc_table(lmscale_ctx* ctx, float** table_out, int64_t*
   return LMSCALE_OK;
 }
 
+lmscale_status lmscale_set_codec(lmscale_ctx* ctx, int32_t codec) {
+  if (!ctx) return LMSCALE_ERR_INVALID_ARG;
+  if (codec != LMSCALE_CODEC_FP16 && codec != LMSCALE_CODEC_BF16)
+    return fail(ctx, LMSCALE_ERR_INVALID_ARG, "unknown codec %d", codec);
+  if (ctx->gexec) {  // a captured step carries the old codec
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  ctx->cbf = codec == LMSCALE_CODEC_BF16 ? 1 : 0;
+  return LMSCALE_OK;
+}
+
 lmscale_status lmscale_set_compression(lmscale_ctx* ctx, float F) {
   if (!ctx) return LMSCALE_ERR_INVALID_ARG;
   if (!(F >= 0.f) || std::isinf(F))
@@ -446,7 +461,7 @@ static lmscale_status codec_call(lmscale_ctx* ctx, bool down, const void* in, in
   if (!in || !out) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "codec: NULL pointer");
   cudaSetDevice(ctx->cfg.device);
   begin_call(ctx);
-  CK(launch_codec(down, in, n, F, out, ctx->num_sms, S(stream)));
+  CK(launch_codec(down, in, n, F, ctx->cbf, out, ctx->num_sms, S(stream)));
   LAUNCHED(1);
   end_call(ctx);
   return LMSCALE_OK;
@@ -928,7 +943,8 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
                        ctx->cfg.rank, G, ctx->trace,
                        table == ctx->table_ptr ? ctx->table_win : nullptr, ctx->lbits_off,
-                       comp ? ctx->cF : 0.f, ctx->mhat_off, ctx->lrank_off, local_m ? 1 : 0, s);
+                       comp ? ctx->cF : 0.f, ctx->cbf, ctx->mhat_off, ctx->lrank_off,
+                       local_m ? 1 : 0, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {

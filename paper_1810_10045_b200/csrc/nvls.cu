@@ -63,10 +63,10 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 __device__ __forceinline__ float add4(float a, float b) { return a + b; }
-__device__ __forceinline__ float4 dech(uint2 u, float F) { return dec4(u, F); }
-__device__ __forceinline__ float dech(__half h, float F) { return dec1(h, F); }
-__device__ __forceinline__ uint2 ench(float4 v, float F) { return enc4(v, F); }
-__device__ __forceinline__ __half ench(float v, float F) { return enc1(v, F); }
+__device__ __forceinline__ float4 dech(uint2 u, float F, int bf) { return dec4(u, F, bf); }
+__device__ __forceinline__ float dech(uint16_t h, float F, int bf) { return dec1(h, F, bf); }
+__device__ __forceinline__ uint2 ench(float4 v, float F, int bf) { return enc4(v, F, bf); }
+__device__ __forceinline__ uint16_t ench(float v, float F, int bf) { return enc1(v, F, bf); }
 
 }  // namespace
 
@@ -86,6 +86,7 @@ struct NvlsKernelArgs {
   ncclWindow_t twin;  // non-null: the table is in a symmetric window; updated rows are
                       // multicast straight into every replica of E (no copy phase)
   float cF;           // compression scale F (k_p2p_update_c)
+  int cbf;            // codec: 0 binary16, 1 bfloat16
   size_t mhat_off;    // byte offset of the compressed M^ rows in the M window
   size_t lrank_off;   // local-slot layout: byte offset of lrank in the window
   int local_m;        // 1: M_j rows are at rank j's local index (lrank + popcount), else at r
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
 template <typename T>
 __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a) {
   constexpr int W = sizeof(T) / sizeof(float);
-  using H = typename std::conditional<W == 4, uint2, __half>::type;
+  using H = typename std::conditional<W == 4, uint2, uint16_t>::type;
   constexpr int MAXG = 8;
   ncclCoopCta cta;
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
@@ -344,13 +345,13 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
             if (c + 32 * q < C) v[q] = pm[j][lrow[j] + c + 32 * q];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (c + 32 * q < C) m[q] = add4(m[q], dech(v[q], F));  // rank order, fp32
+            if (c + 32 * q < C) m[q] = add4(m[q], dech(v[q], F, a.cbf));  // rank order, fp32
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (c + 32 * q < C) {
-          const H e = ench(m[q], F);
+          const H e = ench(m[q], F, a.cbf);
 #pragma unroll
           for (int j = 0; j < MAXG; ++j)
             if (j < a.world) pq[j][mrow + c + 32 * q] = e;
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
         }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (c + 32 * q < C) er[c + 32 * q] = fma4(-a.lr, dech(v[q], F), e[q]);
+        if (c + 32 * q < C) er[c + 32 * q] = fma4(-a.lr, dech(v[q], F, a.cbf), e[q]);
     }
   }
 }
@@ -472,9 +473,10 @@ void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w) {
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
-                        float cF, size_t mhat_off, size_t lrank_off, int local_m,
+                        float cF, int cbf, size_t mhat_off, size_t lrank_off, int local_m,
                         cudaStream_t s) {
   NvlsKernelArgs a;
+  a.cbf = cbf;
   a.lrank_off = lrank_off;
   a.local_m = local_m;
   a.lbits_off = lbits_off;

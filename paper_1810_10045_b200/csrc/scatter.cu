@@ -59,14 +59,14 @@ constexpr unsigned FULL_MASK = 0xffffffffu;
 // (the payload of the compressed exchange) when a.m16.
 __device__ __forceinline__ void st_m(const ScatterArgs& a, size_t slot, int C, int col, float4 v) {
   if (a.m16) {
-    reinterpret_cast<uint2*>(a.M)[slot * C + col] = enc4(v, a.cF);
+    reinterpret_cast<uint2*>(a.M)[slot * C + col] = enc4(v, a.cF, a.cbf);
   } else {
     st_v4(reinterpret_cast<float4*>(a.M) + slot * C + col, v);
   }
 }
 __device__ __forceinline__ void st_m(const ScatterArgs& a, size_t slot, int C, int col, float v) {
   if (a.m16)
-    reinterpret_cast<__half*>(a.M)[slot * C + col] = enc1(v, a.cF);
+    reinterpret_cast<uint16_t*>(a.M)[slot * C + col] = enc1(v, a.cF, a.cbf);
   else
     a.M[slot * C + col] = v;
 }
@@ -767,28 +767,28 @@ namespace lms {
 // ------------------------------------------------------------ codec (R15)
 // q[i] = binary16 bits of RNE(fp32(F * x[i])), saturated.
 __global__ void __launch_bounds__(256) k_compress(const float* __restrict__ x, int64_t n, float F,
-                                                  __half* __restrict__ q) {
+                                                  int bf, uint16_t* __restrict__ q) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    q[i] = enc1(__ldcs(x + i), F);
+    q[i] = enc1(__ldcs(x + i), F, bf);
 }
 // x[i] = fp32(q[i]) / F.
-__global__ void __launch_bounds__(256) k_decompress(const __half* __restrict__ q, int64_t n,
-                                                    float F, float* __restrict__ x) {
+__global__ void __launch_bounds__(256) k_decompress(const uint16_t* __restrict__ q, int64_t n,
+                                                    float F, int bf, float* __restrict__ x) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = dec1(q[i], F);
+    x[i] = dec1(q[i], F, bf);
 }
 
-cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, void* out, int num_sms,
-                         cudaStream_t s) {
+cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, int bf, void* out,
+                         int num_sms, cudaStream_t s) {
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   if (blocks < 1) blocks = 1;
   if (down)
-    k_compress<<<(unsigned)blocks, 256, 0, s>>>((const float*)in, n, F, (__half*)out);
+    k_compress<<<(unsigned)blocks, 256, 0, s>>>((const float*)in, n, F, bf, (uint16_t*)out);
   else
-    k_decompress<<<(unsigned)blocks, 256, 0, s>>>((const __half*)in, n, F, (float*)out);
+    k_decompress<<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)in, n, F, bf, (float*)out);
   return cudaGetLastError();
 }
 }  // namespace lms

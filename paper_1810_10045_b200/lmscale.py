@@ -88,6 +88,7 @@ _plan_seeds = _sig("lmscale_plan_seeds", _S, [ctypes.c_int32, ctypes.c_int32, ct
 _draw_samples = _sig("lmscale_draw_samples", _S, [_P, ctypes.c_uint64, ctypes.c_uint64, _i64, _P,
                                                   _P])
 _lookup = _sig("lmscale_lookup", _S, [_P, _P, _i64, _P, _P, _P])
+_set_codec = _sig("lmscale_set_codec", _S, [_P, ctypes.c_int32])
 _set_compression = _sig("lmscale_set_compression", _S, [_P, ctypes.c_float])
 _compress = _sig("lmscale_compress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
 _decompress = _sig("lmscale_decompress", _S, [_P, _P, _i64, ctypes.c_float, _P, _P])
@@ -101,7 +102,7 @@ EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_u
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
             "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
             "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing", "lmscale_alloc_table",
-            "lmscale_set_compression", "lmscale_compress", "lmscale_decompress",
+            "lmscale_set_compression", "lmscale_set_codec", "lmscale_compress", "lmscale_decompress",
             "lmscale_plan_seeds", "lmscale_draw_samples", "lmscale_lookup", "lmscale_get_stats",
             "lmscale_status_string", "lmscale_last_error", "lmscale_version"]
 
@@ -341,6 +342,10 @@ class Context:
     def set_compression(self, F: float):
         """Sec. 3.3 compressed exchange for later collective steps; 0 = off."""
         self._check(_set_compression(self._h, float(F)), "lmscale_set_compression")
+
+    def set_codec(self, codec: str):
+        """16-bit payload format: "fp16" (binary16, default) or "bf16"."""
+        self._check(_set_codec(self._h, {"fp16": 0, "bf16": 1}[codec]), "lmscale_set_codec")
 
     def compress(self, x, F, stream=None) -> torch.Tensor:
         """binary16 bits (as int16) of RNE(fp32(F * x)), saturated."""

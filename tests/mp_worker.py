@@ -153,7 +153,7 @@ def run_graph_equals_eager(cfg, rank, G, dev, F=0.0):
         print(f"graph==eager G={G} {cfg.name} F={F}", flush=True)
 
 
-def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
+def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False, fmt="fp16"):
     """lmscale_step with compression (Sec. 3.3, R15) against
     oracle.sync_unique_compressed: INT mode bit-exact over the whole table,
     float modes within compressed_tol; replicas bit-identical.  lr is taken
@@ -165,6 +165,7 @@ def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
     E0 = synth.table_values(cfg.V, cfg.D, mode)
     ctx = make_context(cfg.V, cfg.K, cfg.D)
     ctx.set_compression(F)
+    ctx.set_codec(fmt)
     if own_table:
         E = ctx.alloc_table()
         E.copy_(E0.to(dev))
@@ -176,7 +177,7 @@ def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
     torch.cuda.synchronize()
     assert ctx.stats()["fused_s5_s6"] == 3
     Eo = E0.numpy().copy()
-    ref = oracle.sync_unique_compressed(J, [d.numpy() for d in Dh], Eo, lr, F)
+    ref = oracle.sync_unique_compressed(J, [d.numpy() for d in Dh], Eo, lr, F, fmt)
     assert ug == ref["Ug"]
     got = E.cpu().numpy()
     if mode == "int":
@@ -185,7 +186,7 @@ def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
         t = ref["Ihat"].astype(np.int64)
         A = oracle.abs_scale(J, [d.numpy() for d in Dh], ref["Ihat"])
         E0n = E0.numpy()
-        tol = lr * compressed_tol(A, F, G) + 2.0 ** -23 * np.abs(E0n[t])
+        tol = lr * compressed_tol(A, F, G) * (8 if fmt == "bf16" else 1) + 2.0 ** -23 * np.abs(E0n[t])
         check_compressed_rows(got[t], Eo[t], tol, f"compressed G={G} {cfg.name} {mode} F={F}")
         untouched = np.setdiff1d(np.arange(cfg.V), t)
         np.testing.assert_array_equal(got[untouched], E0n[untouched])
@@ -200,7 +201,7 @@ def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False):
     assert ctx.stats()["fused_s5_s6"] in (1, 2)
     check_replicas(E, f"uncompressed after compressed {cfg.name} {mode}")
     if rank == 0:
-        print(f"compressed G={G} {cfg.name} {mode} F={F} own_table={own_table}", flush=True)
+        print(f"compressed G={G} {cfg.name} {mode} F={F} {fmt} own_table={own_table}", flush=True)
     ctx.close()
 
 
@@ -336,6 +337,9 @@ def main():
         run_compressed_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev,
                              1.0)
         run_full(synth.CONFIGS["1b"], rank, G, dev, fused=True, F=1.0)
+        run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "int", rank, G, dev, 1.0, fmt="bf16")
+        run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "signed", rank, G, dev, 1.0,
+                             own_table=True, fmt="bf16")
     for name in ("1b", "char", "amazon", "tieba"):
         if name in which:
             run_full(synth.CONFIGS[name], rank, G, dev)

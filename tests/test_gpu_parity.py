@@ -401,8 +401,9 @@ def test_full_size_emulated_ranks_integers_and_sampled_rows(lm, name, G):
 
 # ------------------------------------------------------------ compression
 
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
 @pytest.mark.parametrize("F", [1.0, 3.0, 256.0, 1024.0])
-def test_codec_bit_exact(lm, F):
+def test_codec_bit_exact(lm, F, fmt):
     """lmscale_compress / lmscale_decompress (R15) against the
     oracle codec, element by element, including subnormals, ties and
     saturation; decompress over every finite binary16 bit pattern."""
@@ -414,14 +415,20 @@ def test_codec_bit_exact(lm, F):
         rng.integers(-4096, 4096, 20_000).astype(np.float32) + 0.5,
         np.float32([0.0, -0.0, 2.0 ** -25, -(2.0 ** -25), 65504.0, 65520.0, 1e30, -1e30]),
     ])
+    if fmt == "bf16":
+        x = np.concatenate([x, np.float32([3.4e38, -3.4e38, 1e-40, 1 + 3 * 2**-8])])
     ctx = lm.Context(16, 16, 4)
+    ctx.set_codec(fmt)
     q = ctx.compress(torch.from_numpy(x).to(dev()), F)
     torch.cuda.synchronize()
-    np.testing.assert_array_equal(q.cpu().numpy().view(np.uint16), oracle.compress(x, F))
+    np.testing.assert_array_equal(q.cpu().numpy().view(np.uint16), oracle.compress(x, F, fmt))
     bits = np.arange(1 << 16, dtype=np.uint16)
-    bits = bits[np.isfinite(bits.view(np.float16))]
+    if fmt == "fp16":
+        bits = bits[np.isfinite(bits.view(np.float16))]
+    else:
+        bits = bits[np.isfinite((bits.astype(np.uint32) << 16).view(np.float32))]
     back = ctx.decompress(torch.from_numpy(bits.view(np.int16)).to(dev()), F)
-    np.testing.assert_array_equal(back.cpu().numpy(), oracle.decompress(bits, F))
+    np.testing.assert_array_equal(back.cpu().numpy(), oracle.decompress(bits, F, fmt))
     assert ctx.compress(torch.empty(0, device=dev()), F).numel() == 0
     with pytest.raises(lm.LmscaleError):
         ctx.compress(torch.ones(4, device=dev()), 0.0)
