@@ -1,5 +1,6 @@
 // coop.cu -- S1 (local unique, step 1) and S3 (global unique +
-// remap, step 4) as ONE cooperative launch each.
+// remap, step 4) as ONE launch each: a normal launch sized to
+// co-residency, phases separated by an in-kernel grid barrier.
 //
 // Both steps touch at most a few MB (ids, bitmaps), so they are bound by
 // latency, not bandwidth: a chain of dependent launches or a serial

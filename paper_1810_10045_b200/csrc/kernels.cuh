@@ -155,7 +155,7 @@ struct ScatterArgs {
   int64_t ug_cap;         // capacity bound on U_g (sizes the grid)
   int num_sms;
 };
-// One cooperative launch: scatter, cut-run fixup, and (a.table) the world-1 S6.
+// One launch: scatter, cut-run fix-up, and (a.apply) the world-1 S6.
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
 // forward lookup: out[p] = E[ids[p]] (zero row for an id >= vocab)
 cudaError_t launch_lookup(const float* table, int D, const uint32_t* ids, int64_t n,

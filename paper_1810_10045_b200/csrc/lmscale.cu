@@ -192,7 +192,8 @@ void end_call(lmscale_ctx* c) {
   c->stats.kernels_total_lo = (int32_t)(c->kernels_total & 0x7fffffff);
 }
 
-// S1 on stream s: one cooperative launch (radix sort + run flags).
+// S1 on stream s: one launch (radix sort + run flags): a thread-
+// block cluster for K <= 64K, else a persistent grid with in-kernel barriers.
 lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t* nu_out,
                       cudaStream_t s, bool world1 = false) {
   S1Args a;
@@ -246,7 +247,7 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   return LMSCALE_OK;
 }
 
-// S3 on stream s: one cooperative launch (bitmap, scan, I^, U_g,
+// S3 on stream s: one launch (bitmap, scan, I^, U_g,
 // and the l2g map of the last S1, which must be complete on `s`).
 lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream_t s,
                       bool peer = false) {
@@ -274,7 +275,7 @@ lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream
   a.bar = ctx->bars + 2;
   CK(launch_s3(a, ctx->num_sms, s));
   LAUNCHED(1);
-  ctx->last_n = n;
+  ctx->last_n = peer ? (int64_t)ctx->cfg.world * ctx->last_k : n;  // I has G*k ids either way
   ctx->have_s3 = true;
   return LMSCALE_OK;
 }
@@ -344,7 +345,7 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   return a;
 }
 
-// S4 (+ the world-1 S6 when table != nullptr): one cooperative launch.
+// S4 (+ the world-1 S6 when apply): one launch.
 lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
                       float* table = nullptr, float lr = 0.f, bool fill_absent = true,
                       float m16_F = 0.f, bool apply = false, bool local_slots = false) {
