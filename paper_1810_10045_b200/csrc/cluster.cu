@@ -38,6 +38,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_s1_cluster(S1Args a) {
   constexpr int CL_TILE = CL_THREADS * IT;
   extern __shared__ uint32_t sm[];
   __shared__ uint32_t s_scan[32];
+  // programmatic dependent launch: the next kernel on the stream (S4) may be
+  // scheduled now; it waits in griddepcontrol.wait until this grid completes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ uint32_t s_heads, s_rtot, s_roff;
   cg::cluster_group cl = cg::this_cluster();
   const int cr = (int)cl.block_rank();

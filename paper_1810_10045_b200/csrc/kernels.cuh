@@ -135,6 +135,7 @@ struct ScatterArgs {
   int fix_cap;
   int fx_last;            // 1: last-arriver fix-up (no grid barrier); 0: listed fix-up phase
   int fxp;                // last-arriver fix-up: partials per part
+  int pdl;                // launched as a programmatic dependent of the S1 kernel before it
   uint32_t* fxcnt;        // last-arriver counters: parts [fx_stride], runs [fx_stride]
   int64_t fx_stride;      // nchunks x column blocks
   int zero_rows;          // 0: every slot is present locally (world 1): slot = local index

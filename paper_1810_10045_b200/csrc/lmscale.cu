@@ -325,6 +325,7 @@ ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
   a.fx_last = fx_barrier ? 0 : 1;
   static const int fxp = getenv("LMSCALE_S4_FXP") ? atoi(getenv("LMSCALE_S4_FXP")) : 32;
   a.fxp = fxp > 0 ? fxp : 32;
+  a.pdl = 0;
   a.fxcnt = ctx->fxcnt;
   a.fx_stride = ctx->fx_stride;
   a.zero_rows = ctx->cfg.world > 1 ? 1 : 0;  // world 1: slot = local index
@@ -354,6 +355,10 @@ lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
   a.table = table;
   a.lr = lr;
   a.apply = apply ? 1 : 0;
+  // world 1: S4 directly follows the cluster S1 on the same stream -- launch
+  // it as a programmatic dependent (its launch overlaps S1's tail)
+  static const bool no_pdl = getenv("LMSCALE_NO_PDL") != nullptr;
+  a.pdl = (apply && !no_pdl && ctx->sorted_keys == nullptr) ? 1 : 0;
   a.fill_absent = fill_absent ? 1 : 0;
   a.m16 = m16_F > 0.f ? 1 : 0;
   a.cF = m16_F;

@@ -498,6 +498,9 @@ __global__ void __launch_bounds__(SC_THREADS, (PRE || FXL) ? 1 : 2) k_scatter(Sc
     atomicMax(a.trace + 63, ~t);
   }
   __shared__ T red[SC_THREADS / 32][32 * NV];
+  // launched as a programmatic dependent of S1: wait for S1's grid to
+  // complete (and its memory to be visible) before reading its outputs
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   // an id >= vocab: no table row is touched (the error surfaces at the next
   // host sync); every CTA reads the same flag, so all leave together
   if (a.apply && (__ldcg(&a.sc3->err) & 1u)) return;
@@ -622,6 +625,18 @@ static cudaError_t scatter_t(const ScatterArgs& a, cudaStream_t s) {
   if (blocks < a.num_sms) blocks = a.num_sms < cap ? a.num_sms : cap;  // phases 2/3 want a wide grid
   // grid <= occupancy x SMs: every CTA is co-resident, so the in-kernel
   // grid barrier is safe with a normal launch
+  if (a.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(SC_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_scatter<T, NV, UNR, PRE, FXL>, a);
+  }
   k_scatter<T, NV, UNR, PRE, FXL><<<(unsigned)blocks, SC_THREADS, 0, s>>>(a);
   return cudaGetLastError();
 }
