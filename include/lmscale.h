@@ -64,12 +64,17 @@ typedef enum {
   LMSCALE_ERR_CUDA = 3,        /* CUDA runtime error (message: lmscale_last_error) */
   LMSCALE_ERR_NCCL = 4,        /* NCCL error or asynchronous communicator error */
   LMSCALE_ERR_OOM = 5,         /* workspace allocation failed */
-  LMSCALE_ERR_UNSUPPORTED = 6  /* e.g. a collective call on a LMSCALE_FLAG_NO_COMM context */
+  LMSCALE_ERR_UNSUPPORTED = 6, /* e.g. a collective call on a LMSCALE_FLAG_NO_COMM context */
+  LMSCALE_ERR_CONSISTENCY = 7  /* LMSCALE_FLAG_CHECK: U_g or the I^ checksum differs across ranks
+                                  (S:268); every rank returns it */
 } lmscale_status;
 
 /* Context flags. */
 #define LMSCALE_FLAG_NO_COMM 1u /* no NCCL communicator: staged calls only (test emulation of G ranks) */
 #define LMSCALE_FLAG_TIMING 2u  /* record CUDA events around each phase; lmscale_get_stats reports them */
+#define LMSCALE_FLAG_CHECK 8u   /* debug: after S3 of every collective call, all-gather (U_g, a
+                                   checksum of I^) and compare across ranks: one host
+                                   sync per call; disables graph capture */
 #define LMSCALE_FLAG_GRAPH 4u   /* lmscale_step captures the whole step into a CUDA graph (once per
                                    (ids, grad, table, k, lr) tuple) and replays it; applies with
                                    num_unique_out == NULL (no host round trip) and either

@@ -158,6 +158,9 @@ struct ScatterArgs {
 };
 // One launch: scatter, cut-run fix-up, and (a.apply) the world-1 S6.
 cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
+// debug consistency check: out[0] = U_g, out[1] = checksum of I^
+cudaError_t launch_checksum(const uint32_t* ihat, const Sc3* sc3, unsigned long long* out,
+                            cudaStream_t s);
 // forward lookup: out[p] = E[ids[p]] (zero row for an id >= vocab)
 cudaError_t launch_lookup(const float* table, int D, const uint32_t* ids, int64_t n,
                           uint32_t vocab, float* out, int num_sms, cudaStream_t s);

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "../../include/lmscale.h"
 #include "common.cuh"
@@ -79,6 +80,7 @@ struct lmscale_ctx {
   char* peer_base[8] = {};     // LSA base of every rank's M window
   bool peer_s3 = false;        // S3 ORs the peers' local bitmaps (no ID all-gather)
   uint32_t* s3_epoch = nullptr;
+  void* ck_dev = nullptr;      // FLAG_CHECK scratch: (U_g, checksum) x (1 + world)
   float cF = 0.f;              // compression scale (0: off), lmscale_set_compression
   int cbf = 0;                 // codec: 0 binary16, 1 bfloat16 (lmscale_set_codec)
   GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
@@ -399,6 +401,7 @@ const char* lmscale_status_string(lmscale_status s) {
     case LMSCALE_ERR_NCCL: return "NCCL error";
     case LMSCALE_ERR_OOM: return "out of device memory";
     case LMSCALE_ERR_UNSUPPORTED: return "unsupported on this context";
+    case LMSCALE_ERR_CONSISTENCY: return "U_g or I^ differs across ranks";
   }
   return "unknown status";
 }
@@ -583,7 +586,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
            o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
            o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
            o_bT = take(4 * (size_t)ctx->ntiles_max * (1u << ctx->plan.bits)),
-           o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W), o_epoch = take(64);
+           o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W), o_epoch = take(64),
+           o_ck = take(16 * (size_t)(cfg->world + 1));
     // M lives in its own allocation: with a communicator it comes from
     // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
     // (+256: room to align the compressed M^ region at byte 2*ucap*D)
@@ -623,6 +627,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
     ctx->s3_epoch = (uint32_t*)(b + o_epoch);
+    ctx->ck_dev = (void*)(b + o_ck);
     ctx->partial = (float*)(b + o_part);
     ctx->part2 = (float*)(b + o_part2);
     ctx->fxcnt = (uint32_t*)(b + o_fxcnt);
@@ -917,6 +922,24 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     if (st) return st;
   }
   rec(ctx, EV_S3_END, s);
+  if ((ctx->cfg.flags & LMSCALE_FLAG_CHECK) && G > 1 && !ctx->capturing) {
+    // debug: every rank must hold the same U_g and I^
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->ck_dev);
+    CK(launch_checksum(ctx->ihat, ctx->sc3, d, s));
+    LAUNCHED(1);
+    NK(ncclAllGather(d, d + 2, 2, ncclUint64, ctx->comm, s));
+    std::vector<unsigned long long> h(2 * (size_t)(G + 1));
+    CK(cudaMemcpyAsync(h.data(), d, h.size() * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int j = 0; j < G; ++j)
+      if (h[2 + 2 * j] != h[0] || h[3 + 2 * j] != h[1]) {
+        end_call(ctx);
+        return fail(ctx, LMSCALE_ERR_CONSISTENCY,
+                    "rank %d: U_g %llu checksum %llx, rank %d: U_g %llu checksum %llx",
+                    ctx->cfg.rank, h[0], h[1], j, h[2 + 2 * j], h[3 + 2 * j]);
+      }
+  }
   // The host reads {U_g, err, U_i} only when it must: for NCCL's element count
   // (G > 1 without the fused NVLS kernel) or when the caller asks for U_g.
   const bool host_reads = need_host_ug || !(table && (G == 1 || ctx->nvls));
@@ -1069,7 +1092,8 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
   // when world > 1 runs the peer-bitmap S3 and a fused S5+S6 kernel (no NCCL
   // host calls at all), so it is captured once per argument tuple and
   // replayed (one launch instead of 3-4 kernels + events).
-  if (ctx && (ctx->cfg.flags & LMSCALE_FLAG_GRAPH) && !num_unique_out &&
+  if (ctx && (ctx->cfg.flags & LMSCALE_FLAG_GRAPH) && !(ctx->cfg.flags & LMSCALE_FLAG_CHECK) &&
+      !num_unique_out &&
       (ctx->cfg.world == 1 || (ctx->peer_s3 && ctx->nvls))) {
     lmscale_status st0 = check_ids_args(ctx, ids, k);
     if (st0) return st0;

@@ -809,6 +809,39 @@ cudaError_t launch_codec(bool down, const void* in, int64_t n, float F, int bf, 
 }  // namespace lms
 
 namespace lms {
+// ------------------------------------------- consistency check (debug)
+// out[0] = U_g, out[1] = sum over r < U_g of mix(I^[r] + r * 2^32): every
+// rank computes I^ redundantly, so the pairs must agree everywhere.
+__device__ __forceinline__ uint64_t ck_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void __launch_bounds__(1024) k_checksum(const uint32_t* __restrict__ ihat,
+                                                   const Sc3* __restrict__ sc3,
+                                                   unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long part[32];
+  const int64_t ug = sc3->u_global;
+  unsigned long long h = 0;
+  for (int64_t r = threadIdx.x; r < ug; r += blockDim.x)
+    h += ck_mix((uint64_t)ihat[r] + ((uint64_t)r << 32));
+  for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = h;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    out[0] = (unsigned long long)ug;
+    out[1] = t;
+  }
+}
+cudaError_t launch_checksum(const uint32_t* ihat, const Sc3* sc3, unsigned long long* out,
+                            cudaStream_t s) {
+  k_checksum<<<1, 1024, 0, s>>>(ihat, sc3, out);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------ forward lookup
 // out[p, :] = E[ids[p], :] -- the input-embedding projection of the K tokens
 // (SURVEY 8(f) row 4).  Warp per row, grid-stride, 128-bit accesses when the

@@ -22,10 +22,11 @@ if not os.path.exists(LIB_PATH):
 
 _lib = ctypes.CDLL(LIB_PATH)
 
-OK, INVALID_ARG, ID_RANGE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED = range(7)
+OK, INVALID_ARG, ID_RANGE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED, CONSISTENCY = range(8)
 FLAG_NO_COMM = 1
 FLAG_TIMING = 2
 FLAG_GRAPH = 4
+FLAG_CHECK = 8
 
 _P = ctypes.c_void_p
 _i64 = ctypes.c_int64

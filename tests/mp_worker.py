@@ -124,6 +124,27 @@ def run_fused_small(cfg, mode, rank, G, dev, own_table=False):
     ctx.close()
 
 
+def run_consistency_check(cfg, rank, G, dev):
+    """LMSCALE_FLAG_CHECK: U_g and the I^ checksum agree on every rank,
+    so the checked step and sync return OK and match an unchecked context."""
+    lr = synth.default_lr("int")
+    ids = torch.from_numpy(synth.ids_for(cfg, rank).view(np.int32)).to(dev)
+    g = synth.grad_values(cfg.K, cfg.D, "int", rank=rank).to(dev)
+    outs = []
+    for flags in (0, lmscale.FLAG_CHECK):
+        ctx = make_context(cfg.V, cfg.K, cfg.D, flags=flags)
+        E = synth.table_values(cfg.V, cfg.D, "int").to(dev)
+        ug = ctx.step(ids, g, E, lr, want_num_unique=True)
+        sg = ctx.sync(ids, g)
+        assert sg.num_unique == ug
+        torch.cuda.synchronize()
+        outs.append(E.cpu())
+        ctx.close()
+    assert torch.equal(outs[0], outs[1])
+    if rank == 0:
+        print(f"consistency check ok G={G} U_g={ug}", flush=True)
+
+
 def run_graph_equals_eager(cfg, rank, G, dev, F=0.0):
     """World > 1 with LMSCALE_FLAG_GRAPH (peer-bitmap S3 + fused S5+S6, no NCCL
     host calls): three captured-and-replayed steps give the same table bits as
@@ -321,6 +342,8 @@ def main():
         run_fused_small(synth.Config("odd", V=3000, K=2500, D=37, G=G), "int", rank, G, dev)
         for mode in ("int", "signed"):
             run_fused_small(synth.CONFIGS["tiny"].with_(G=G), mode, rank, G, dev, own_table=True)
+    if "small" in which:
+        run_consistency_check(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev)
     if "small" in which or "graph" in which:
         run_graph_equals_eager(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev)
         run_graph_equals_eager(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev, F=1.0)

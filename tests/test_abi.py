@@ -45,6 +45,7 @@ def test_binding_names_match_header(lib):
     assert sorted(lmscale.EXPORTED) == declared_functions()
     assert lmscale.version().startswith("lmscale")
     assert lmscale._status_string(2).decode() == "token id >= vocab"
+    assert lmscale._status_string(lmscale.CONSISTENCY).decode() == "U_g or I^ differs across ranks"
 
 
 def test_init_rejects_bad_config_without_touching_gpu(lib):
