@@ -12,6 +12,6 @@ for f in sys.argv[1:]:
         dn = d.get("dense_baseline") or {}
         print(f"{f}: {d['config']['workload']} N={d['n_gpus']} {d['value']/1e6:.1f} Mtok/s "
               f"{d.get('us_per_step', 0):.1f} us/step U_g={d.get('U_global')} phases={ph} "
-              f"S4frac={d.get('roofline', {}).get('frac', 0):.3f} S56frac={(d.get('roofline_s5_s6') or {}).get('frac', 0):.3f} "
+              f"S4frac={d.get('roofline', {}).get('frac', 0):.3f} S56frac={((d.get('roofline_s5_s6') or {}).get('frac') or 0):.3f} "
               f"dense_us={1e3*dn.get('ms_per_step', 0):.1f} speedup={dn.get('speedup_unique_vs_dense', 0):.2f} "
               f"gate={dn.get('gate_0.8x', 0):.2f} e2e={((d.get('e2e') or {}).get('value') or 0)/1e6:.1f}M")
