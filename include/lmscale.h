@@ -113,9 +113,11 @@ typedef struct {
   int64_t workspace_bytes;     /* device bytes owned by the context */
   int32_t kernels_last_call;   /* kernels this library launched in the last call */
   int32_t kernels_total_lo;    /* running count of launched kernels (low 31 bits) */
-  int32_t fused_s5_s6;         /* 1: the last step ran S5+S6 as one NVLS multicast kernel
-                                  (us_allreduce then times that kernel, us_update ~ 0);
-                                  2: same, multicasting straight into the table windows;
+  int32_t fused_s5_s6;         /* 1: the last step ran S5+S6 as one multicast (NVLS) kernel
+                                  with a caller-owned table (us_allreduce then times that
+                                  kernel, us_update ~ 0);
+                                  2: same with the context's table window (peer-to-peer
+                                  kernel for world <= 8: stores into every replica);
                                   3: the compressed (binary16) exchange of
                                   lmscale_set_compression */
   int32_t nvls_available;      /* 1: the context has the multicast window (world > 1) */
@@ -246,10 +248,11 @@ LMSCALE_API lmscale_status lmscale_train_step_host(lmscale_ctx* ctx, const uint3
 
 /* Allocate the vocab x dim fp32 embedding table E on this context's device
  * (owned by the context, freed by lmscale_destroy).  Collective when world > 1
- * and the context has the NVLS multicast window: the table is then allocated
- * with ncclMemAlloc and registered as a symmetric window, and lmscale_step
- * multicasts each updated row straight into every replica of E (no local
- * copy phase).  Any caller-owned table keeps working; this one is faster.
+ * and the context has the symmetric window: the table is then allocated with
+ * ncclMemAlloc and registered as a symmetric window, and lmscale_step's fused
+ * S5+S6 kernel stores each updated row straight into every replica of E over
+ * NVLink (peer-to-peer for world <= 8, multicast above; no local copy phase).
+ * Any caller-owned table keeps working; this one is faster.
  * *bytes_out (host, may be NULL) receives vocab * dim * 4. */
 LMSCALE_API lmscale_status lmscale_alloc_table(lmscale_ctx* ctx, float** table_out /* host */,
                                                int64_t* bytes_out /* host */);
