@@ -284,10 +284,12 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
 //      word I^[r] (peers' presence bitmaps), up-casts, divides by F, sums in
 //      fp32 in rank order, compresses the sum and stores it into every rank's
 //      M^ region (P2P stores, half the bytes of fp32 rows);
+//      (the owner also updates its own E row right away from the decoded
+//      compressed sum, the value every other rank will apply);
 //   3. LSA barrier: every compressed row of M^ has landed;
-//   4. every rank updates all U_g rows of its own E from its local M^:
-//      E[I^[r]] = fma(-lr, dec(M^[r]), E[I^[r]]) -- the same instruction on the
-//      same bits on every rank, so the replicas stay bit-identical.
+//   4. every rank updates the other ranks' rows of its own E from its local
+//      M^: E[I^[r]] = fma(-lr, dec(M^[r]), E[I^[r]]) -- the same instruction on
+//      the same bits on every rank, so the replicas stay bit-identical.
 // Per GPU and direction: (G-1)/G x (present rows + U_g rows) x 2 bytes x D.
 template <typename T>
 __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a) {
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
     pb[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
     pr[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
   }
+  T* Eo = reinterpret_cast<T*>(a.table);
   for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
     const int64_t r = a.rank + a.world * t;
     const uint32_t w = __ldg(a.ihat + r);
@@ -332,10 +335,14 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
           lrow[j] = (size_t)(__ldcg(pr[j] + (w >> 5)) + __popc(bits & ((1u << (w & 31u)) - 1u))) * C;
       }
     }
+    T* er = Eo + (size_t)w * C;  // this rank's own row of E (updated here, not in phase 2)
     for (int c = lane; c < C; c += 128) {
-      T m[4];
+      T m[4], ev[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) m[q] = T{};
+      for (int q = 0; q < 4; ++q) {
+        m[q] = T{};
+        if (c + 32 * q < C) ev[q] = er[c + 32 * q];
+      }
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
         if ((has >> j) & 1u) {
@@ -354,7 +361,9 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
           const H e = ench(m[q], F, a.cbf);
 #pragma unroll
           for (int j = 0; j < MAXG; ++j)
-            if (j < a.world) pq[j][mrow + c + 32 * q] = e;
+            if (j < a.world && j != a.rank) pq[j][mrow + c + 32 * q] = e;
+          // the owner applies the same decoded value every other rank applies
+          er[c + 32 * q] = fma4(-a.lr, dech(e, F, a.cbf), ev[q]);
         }
       }
     }
@@ -364,7 +373,8 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
   T* E = reinterpret_cast<T*>(a.table);
   // rows in the same (owner, t) order as phase 1: the barrier above is per
   // CTA index, so CTA k may only read the rows that CTAs k wrote
-  for (int j = 0; j < a.world; ++j)
+  for (int j = 0; j < a.world; ++j) {
+  if (j == a.rank) continue;  // own rows were updated in phase 1
   for (int64_t t = gw; j + a.world * t < Ug; t += nw) {
     const int64_t r = j + a.world * t;
     T* er = E + (size_t)__ldg(a.ihat + r) * C;
@@ -382,6 +392,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
       for (int q = 0; q < 4; ++q)
         if (c + 32 * q < C) er[c + 32 * q] = fma4(-a.lr, dech(v[q], F, a.cbf), e[q]);
     }
+  }
   }
 }
 
