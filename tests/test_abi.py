@@ -76,3 +76,18 @@ def test_plan_seeds_host_logic_matches_oracle(lib, policy):
         assert got == (want[0], want[1]), (G, policy)
     with pytest.raises(lmscale.LmscaleError):
         lmscale.plan_seeds(8, "power", 1.5)
+
+
+def test_product_path_never_touches_the_oracle():
+    """The product package (paper_1810_10045_b200/: binding + CUDA sources)
+    neither imports nor links the CPU oracle, and the binding has no CPU
+    fallback: it loads liblmscale.so or raises."""
+    import pathlib
+    import re
+    pkg = pathlib.Path(__file__).resolve().parent.parent / "paper_1810_10045_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        text = f.read_text()
+        assert not re.search(r"^\s*(import|from)\s+oracle", text, re.M), f
+        assert "liboracle" not in text and "oracle_" not in text, f
+    binding = (pkg / "lmscale.py").read_text()
+    assert "CDLL" in binding
