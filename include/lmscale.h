@@ -96,8 +96,10 @@ typedef struct {
 typedef struct {
   const uint32_t* ids; /* device, I^ ascending, num_unique entries */
   float* rows;         /* device, num_unique x dim row-major: M^ after a collective sync,
-                          this rank's M_g after lmscale_scatter_expand */
-  int64_t num_unique;  /* host value U_g */
+                          this rank's M_g after lmscale_scatter_expand;
+                          NULL after an lmscale_step that consumed the rows (S6 folded
+                          into S4 at world 1, or the fused S5+S6 kernel) */
+  int64_t num_unique;  /* host value U_g (-1 when the step kept it on the device) */
 } lmscale_sparse_grad;
 
 typedef struct {
