@@ -91,15 +91,21 @@ typedef struct {
   uint32_t flags;     /* LMSCALE_FLAG_* */
 } lmscale_config;
 
-/* The synchronised sparse gradient: a borrowed view into the context's
- * workspace, valid until the next call on the same context that runs S1-S5. */
+/* The synchronised sparse gradient: a borrowed view into the
+ * context's workspace, valid until the next call on the same context that
+ * runs S1-S5. */
 typedef struct {
-  const uint32_t* ids; /* device, I^ ascending, num_unique entries */
-  float* rows;         /* device, num_unique x dim row-major: M^ after a collective sync,
-                          this rank's M_g after lmscale_scatter_expand;
-                          NULL after an lmscale_step that consumed the rows (S6 folded
-                          into S4 at world 1, or the fused S5+S6 kernel) */
-  int64_t num_unique;  /* host value U_g (-1 when the step kept it on the device) */
+  const uint32_t* ids;   /* device, I^ ascending, num_unique entries */
+  const int32_t* counts; /* device, num_unique entries: tokens of word I^[r] over all ranks
+                            (the global counts of step 4) after lmscale_sync_embedding_grad
+                            (and lmscale_get_sparse_grad after it); NULL after the staged
+                            calls and after lmscale_step, which do not compute them */
+  float* rows;           /* device, num_unique x dim row-major: M^ after a collective sync,
+                            this rank's M_g after lmscale_scatter_expand;
+                            NULL after an lmscale_step that consumed the rows (S6 folded
+                            into S4 at world 1, or the fused S5+S6 kernel), also from
+                            lmscale_get_sparse_grad */
+  int64_t num_unique;    /* host value U_g (-1 when the step kept it on the device) */
 } lmscale_sparse_grad;
 
 typedef struct {
@@ -107,11 +113,14 @@ typedef struct {
   int64_t u_global; /* U_g of the last S3 */
   /* per-phase device time of the last collective sync, microseconds (FLAG_TIMING; else -1) */
   double us_dedup, us_gather, us_merge, us_scatter, us_allreduce, us_update, us_total;
-  /* per-step byte accounting of the last sync (SURVEY Sec. 8(d) algorithmic bytes) */
-  int64_t bytes_ids_gathered;  /* 4 (G-1) K ingress */
-  int64_t bytes_grad_allreduce;/* 4 U_g D payload */
-  int64_t bytes_scatter;       /* 4 K D read + 4 U_g D written */
-  int64_t bytes_update;        /* 12 U_g D */
+  /* per-rank byte accounting of the last lmscale_step / sync / host step, for
+     the kernels that ran (SURVEY Sec. 8(d) algorithmic bytes; filled on every
+     path, U_g read back from the device if the step kept it there): */
+  int64_t bytes_ids_gathered;  /* S2 ingress: 4 (G-1) K ids, or 4 ceil(V/32) (G-1) bitmap words */
+  int64_t bytes_grad_allreduce;/* S5 payload: 4 U_g D (2 U_g D compressed); 0 at world 1 */
+  int64_t bytes_scatter;       /* S4: 4 K D read + rows written (4 U_g D; local-slot layout
+                                  4 U_i D; world-1 fold: 8 U_g D, each E row read + written) */
+  int64_t bytes_update;        /* separate S6 launch: 12 U_g D; 0 when folded or fused */
   int64_t workspace_bytes;     /* device bytes owned by the context */
   int32_t kernels_last_call;   /* kernels this library launched in the last call */
   int32_t kernels_total_lo;    /* running count of launched kernels (low 31 bits) */

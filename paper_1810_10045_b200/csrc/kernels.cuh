@@ -9,16 +9,6 @@ namespace lms {
 
 struct GridBar;
 
-// Scatter-add chunk: sorted positions per warp work item.
-constexpr int SC_CHUNK = 32;
-// Fix-up: partial rows summed per CTA work item.
-constexpr int FX_PART = 128;
-// Runs of <= FX_SHORT tokens are summed whole by the chunk holding their start
-// (<= SC_CHUNK: the read-on past a chunk edge stays within one more chunk).
-constexpr int FX_SHORT = 32;
-// Zero-row group: slots per warp work item.
-constexpr int SC_ZGROUP = 32;
-
 // Per-step device scalars of S1 (zeroed at the start of S1).
 struct Sc1 {
   int64_t u_local;
@@ -32,47 +22,10 @@ struct Sc3 {
   uint32_t pad;
 };
 
-struct SortPlan {
-  int passes;
-  int bits;  // digit width per pass
-};
-
-// ---- cooperative S1 / S3 (coop.cu) -----------------------------------------
+// ---- S3 (coop.cu) ----------------------------------------------------------
 constexpr int CO_THREADS = 512;
-constexpr int CO_ITEMS = 8;
-constexpr int CO_TILE = CO_THREADS * CO_ITEMS;  // 4096 keys per tile
-constexpr int CO_MAX_BITS = 11;                 // <= 2048 digits per pass
-constexpr int CO_HOTW = 2048;                   // shared-memory bitmap words in S3
+constexpr int CO_HOTW = 2048;  // shared-memory bitmap words in S3
 
-struct S1Args {
-  const uint32_t* ids;
-  int K;
-  uint32_t vocab;
-  int passes, bits;
-  uint32_t *ka, *kb;
-  int32_t *va, *vb;
-  uint32_t* cT;  // [passes][1 << bits][ntp] digit-major per-tile counts
-  uint32_t* bT;  // [ntiles][1 << bits] tile-major bases (one pass at a time)
-  uint32_t* rtot;  // [grid] digit-range totals
-  int ntiles, ntp;
-  uint32_t* luniq;
-  int32_t* lstart;
-  int32_t* segidx;
-  int32_t* inverse;
-  uint32_t* lbits;
-  uint32_t* lrank;  // optional: lrank[w] = local index of the first present id of word w
-  int64_t W;
-  uint32_t* heads;  // [ntiles]
-  Sc1* sc;
-  int64_t* nu_out;
-  unsigned long long* trace;  // optional phase timestamps (LMSCALE_PHASE_TRACE)
-  // world == 1 shortcut (I = J, so I^ = J^, U_g = U_i, l2g = identity): when
-  // non-null, S1 also writes I^, l2g and the S3 scalars and S3 is skipped.
-  uint32_t* ihat;
-  int32_t* l2g;
-  Sc3* sc3;
-  GridBar* bar;  // in-kernel grid barrier (cooperative-size grid, normal launch)
-};
 struct S3Args {
   const uint32_t* I;
   int64_t n;
@@ -98,66 +51,103 @@ struct S3Args {
   size_t flags_off;     // byte offset of the per-rank arrival flags (world words)
   uint32_t* epoch;      // local step counter of the handshake (device)
 };
-SortPlan make_coop_plan(uint64_t vocab);
 
-// ---- cluster S1 (cluster.cu): K <= CL_MAX_CTAS * CL_MAX_TILE, one cluster --
-constexpr int CL_THREADS = 512;
-constexpr int CL_MAX_TILE = 4096;  // keys per CTA (512 threads x 8)
-constexpr int CL_MAX_BITS = 10;
-constexpr int CL_MAX_CTAS = 16;
-SortPlan make_cluster_plan(uint64_t vocab);
-size_t cluster_smem_bytes(int bits);
-bool cluster_s1_ok(int K);
-// Writes the stable permutation to a.va (a.ka/a.kb/a.vb unused).
-cudaError_t launch_s1_cluster(const S1Args& a, cudaStream_t s);
-size_t s1_smem_bytes(int bits);
-cudaError_t launch_s1(const S1Args& a, int num_sms, cudaStream_t s);
 cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s);
+// Global counts of I^ (gcounts[r] = tokens of word I^[r] over all ranks):
+// peer_base != nullptr: from every rank's S1 counts in its window (lbits,
+// lrank, counts at the given offsets); else from the gathered ids I (n).
+cudaError_t launch_gcounts(int32_t* gcounts, int64_t ucap, const uint32_t* ihat, const Sc3* sc3,
+                           const uint32_t* I, int64_t n, const uint32_t* gbits,
+                           const uint32_t* wrank, uint32_t vocab, int world,
+                           char* const* peer_base, size_t lbits_off, size_t lrank_off,
+                           size_t counts_off, int num_sms, cudaStream_t s);
+
+// ---- S1 grouping (group.cu): one launch, three grid barriers ----------------
+constexpr int G1_THREADS = 512;
+constexpr int G1_MAX_GRID = 1024;
+constexpr int G1_STRIPES = 16;
+struct G1Args {
+  const uint32_t* ids;
+  int K;
+  uint32_t vocab;
+  uint32_t* wcount;   // [32 W] tokens per id (transposed layout); all zero between launches
+  uint32_t* tick;     // [K] rank of the token among equal ids (arrival order)
+  uint32_t* lbits;    // [W] presence bitmap; zero on entry unless zero_bits
+  uint32_t* lrank;    // [W] index in J^ of the first present id of each 32-id word
+  int64_t W;
+  uint32_t* ctot;     // [G1_STRIPES][2 * grid] per-range (ids, tokens); zero between launches
+  uint32_t* luniq;    // J^ (U_i)
+  int32_t* counts;    // tokens per word of J^
+  int32_t* lstart;    // first grouped position of each run (U_i + 1)
+  int32_t* perm;      // grouped position -> token position
+  int32_t* inverse;   // token position -> u (-1 for an id >= vocab)
+  int32_t* runfirst;  // [nr + 1] run holding the first position of each S4 range; [nr] = U_i
+  int nr;             // S4 ranges: [r seg_len, min(K, (r + 1) seg_len))
+  uint32_t seg_len;
+  Sc1* sc;
+  int64_t* nu_out;
+  int zero_bits;
+  unsigned long long* trace;
+  // world 1 (I = J): I^ = J^, l2g = identity, U_g = U_i; S3 is skipped
+  uint32_t* ihat;
+  int32_t* l2g;
+  Sc3* sc3;
+  GridBar* bar;
+};
+cudaError_t launch_group(const G1Args& a, int num_sms, cudaStream_t s);
 
 void launch_counts_export(const int32_t* lstart, const uint32_t* luniq, const int32_t* inverse,
                           const Sc1* sc, int K, int32_t* counts, uint32_t* uniq_out,
                           int32_t* counts_out, int32_t* inverse_out, cudaStream_t s);
 
-// ---- S4 -------------------------------------------------------------------
-struct ScatterArgs {
+// ---- S4 (segsum.cu): bulk-copy-staged segmented sum over equal ranges -------
+constexpr int SEG_MAX_SLOTS = 16;   // mbarrier ring slots (gradient groups, E rows)
+constexpr int SEG_MAX_L = 4096;     // grouped positions per CTA range
+constexpr int SEG_MAX_OCC = 4;      // CTAs per SM
+constexpr int SEG_FXP = 8;          // partial rows of a cut run summed per group
+constexpr int SEG_MAX_THREADS = 544;
+struct SegArgs {
   const float* grad;      // K x D
-  const int32_t* perm;    // sorted position -> token position
-  const int32_t* segidx;  // sorted position -> local unique index u
-  const int32_t* l2g;     // u -> global slot
-  const int32_t* lstart;  // u -> first sorted position (U_i + 1 entries)
-  const uint32_t* ihat;   // slot -> word id
-  const uint32_t* lbits;  // local presence bitmap
-  const Sc3* sc3;         // U_g
-  const Sc1* sc1;         // U_i
-  Sc1* sc1w;              // fixup list counter
-  int2* fixent;           // fix-up entries: (owner chunk, part | nparts << 16)
-  float* part2;           // level-2 partial rows, one per entry (fix_cap x D)
-  int fix_cap;
-  int fx_last;            // 1: last-arriver fix-up (no grid barrier); 0: listed fix-up phase
-  int fxp;                // last-arriver fix-up: partials per part
-  int pdl;                // launched as a programmatic dependent of the S1 kernel before it
-  uint32_t* fxcnt;        // last-arriver counters: parts [fx_stride], runs [fx_stride]
-  int64_t fx_stride;      // nchunks x column blocks
-  int zero_rows;          // 0: every slot is present locally (world 1): slot = local index
-  int fill_absent;        // zero the M rows of slots absent on this rank (world > 1)
-  int m16;                // M rows are stored compressed (binary16 of cF * x, R15)
-  int apply;              // world 1: S6 folded in -- finished rows update `table`, no M
-  float cF;               // compression scale F
-  int cbf;                // codec: 0 binary16, 1 bfloat16
-  int short_runs;         // finish runs <= FX_SHORT in their starting chunk (large K)
-  float* table;           // non-null: world-1 fused S6 (E[I^[r]] -= lr * M[r])
+  const int32_t* perm;    // grouped position -> token position
+  const int32_t* runfirst;  // [nr + 1] run holding each range's first position (S1)
+  const int32_t* lstart;  // u -> first grouped position (U_i + 1 entries)
+  const uint32_t* word;   // u -> word id (world-1 apply: J^ = I^)
+  const int32_t* l2g;     // u -> slot of M (global layout), nullptr: slot = u
+  const Sc1* sc1;         // err
+  float* table;           // apply: E, vocab x D
   float lr;
-  unsigned long long* trace;
-  GridBar* bar;           // in-kernel grid barrier state (zeroed at init)
-  float* M;               // U_g x D
-  float* partial;         // 2 * nchunks x D
-  int K;
-  int D;
-  int64_t ug_cap;         // capacity bound on U_g (sizes the grid)
-  int num_sms;
+  int apply;              // world 1: S6 folded in (E rows updated, no M)
+  float* M;               // slots x D (fp32, or binary16 when m16)
+  int m16;
+  float cF;
+  int cbf;
+  float* part;            // [2 nR] x D partial rows of cut runs
+  float* part2;           // [2 nR] x D group sums of the partial rows
+  uint32_t* cnt;          // [2 nR x ncb] group counters (zero between launches)
+  uint32_t* cnt2;         // [nR x ncb] run counters (zero between launches)
+  uint32_t* lbits;        // clear_bits: zeroed here (world 1)
+  int64_t W;
+  int clear_bits;
+  int pdl;                // launched as a programmatic dependent of S1
+  unsigned long long* trace;  // LMSCALE_PHASE_TRACE stamps (or nullptr)
+  int K, D, num_sms;
+  uint32_t seg_len;       // set by launch_seg: grouped positions per range
+  int cbw, nct, gr, nslot, neslot, lmax;
 };
-// One launch: scatter, cut-run fix-up, and (a.apply) the world-1 S6.
-cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
+struct SegPlan {
+  bool tma;
+  int cbw, nct, threads, ncb, gr, nslot, neslot, occ, nr, lmax;
+  size_t smem;
+};
+SegPlan seg_plan(int64_t K, int64_t D, bool vec, bool apply, int num_sms);
+// the S4 ranges for (K, D): nr ranges of seg_len grouped positions (the last
+// one shorter); S1 writes runfirst for them
+int seg_ranges(int64_t K, int64_t D, int num_sms, uint32_t* seg_len);
+int64_t seg_max_ranges(int64_t K, int num_sms);
+cudaError_t launch_seg(const SegArgs& a, cudaStream_t s);
+cudaError_t launch_zero_absent(float* M, int D, const uint32_t* ihat, const uint32_t* lbits,
+                               const Sc3* sc3, const Sc1* sc1, int64_t ug_cap, int num_sms,
+                               cudaStream_t s);
 // debug consistency check: out[0] = U_g, out[1] = checksum of I^
 cudaError_t launch_checksum(const uint32_t* ihat, const Sc3* sc3, unsigned long long* out,
                             cudaStream_t s);

@@ -45,13 +45,24 @@ enum Ev {
   EV_COUNT
 };
 
+// which kernels the last step ran (for lmscale_get_stats' byte accounting)
+enum PathKind {
+  PATH_NONE = 0,
+  PATH_W1_FOLD,    // world 1: S1 + S4 with S6 folded in
+  PATH_W1_UPDATE,  // world 1: S1 + S4 + k_update
+  PATH_W1_SYNC,    // world 1: S1 + S4 (M returned)
+  PATH_NCCL,       // G > 1: S3 + S4 + ncclAllReduce (+ k_update)
+  PATH_P2P,        // G > 1: fused S5+S6 over NVLink P2P (present rows)
+  PATH_P2P_COMP,   // G > 1: compressed fused S5+S6 (binary16 / bfloat16)
+  PATH_NVLS        // G > 1: fused S5+S6 over NVLS multicast
+};
+
 }  // namespace
 
 struct lmscale_ctx {
   lmscale_config cfg;
   int num_sms = 0;
-  int64_t K = 0, W = 0, NI = 0, ucap = 0, nchunks = 0, ntiles_max = 0, ntp_max = 0;
-  SortPlan plan{}, cl_plan{};
+  int64_t K = 0, W = 0, NI = 0, ucap = 0, nr_max = 0;
   cudaStream_t s_side = nullptr, s_copy = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_s1 = nullptr, ev_s3 = nullptr, ev_copy = nullptr;
   cudaEvent_t ev_s4 = nullptr;
@@ -61,14 +72,13 @@ struct lmscale_ctx {
   // device workspace
   void* base = nullptr;
   size_t ws_bytes = 0;
-  uint32_t *keys_a, *keys_b, *luniq, *lbits, *gbits, *wrank, *I, *ihat, *cT, *heads, *ctot, *bT;
-  int32_t *vals_a, *vals_b, *segidx, *inverse, *lstart, *counts, *l2g;
-  int2* fixent;
-  uint32_t* fxcnt = nullptr;
-  int64_t fx_stride = 0;
-  float* part2;
+  uint32_t *luniq, *lbits, *gbits, *wrank, *I, *ihat, *ctot, *ctot1, *wcount, *tick;
+  int32_t *perm, *runfirst, *inverse, *lstart, *counts, *l2g, *gcounts;
+  float* part = nullptr;       // S4 partial rows of cut runs (2 nr_max x D)
+  float* part2 = nullptr;      // S4 group sums of partial rows (2 nr_max x D)
+  uint32_t* pcnt = nullptr;    // S4 last-arriver counters
+  bool lbits_clean = true;     // the presence bitmap is all zero (S1 may skip clearing it)
   float* M = nullptr;
-  float* partial;
   bool m_nccl = false;
   void* m_reg = nullptr;
   NvlsState* nvls = nullptr;   // fused S5+S6 available
@@ -76,7 +86,8 @@ struct lmscale_ctx {
   size_t mhat_off = 0;         // byte offset of the compressed M^ rows inside the M window
   size_t flags_off = 0;        // byte offset of the S3 handshake flags inside the M window
   size_t lrank_off = 0;        // byte offset of lrank (per-word local base index) in the window
-  uint32_t* lrank = nullptr;   // S1 output for the local-slot M layout (window only)
+  size_t counts_off = 0;       // byte offset of S1's counts in the window
+  uint32_t* lrank = nullptr;   // S1: index in J^ of the first present id of each 32-id word
   char* peer_base[8] = {};     // LSA base of every rank's M window
   bool peer_s3 = false;        // S3 ORs the peers' local bitmaps (no ID all-gather)
   uint32_t* s3_epoch = nullptr;
@@ -101,11 +112,16 @@ struct lmscale_ctx {
   // call state
   int64_t last_k = -1, last_n = -1;
   bool have_s1 = false, have_s3 = false;
-  const uint32_t* sorted_keys = nullptr;
-  const int32_t* sorted_vals = nullptr;
   int64_t last_ug = 0;
+  bool m_consumed = false;       // the last step consumed M (S6 folded / fused S5+S6)
+  bool gcounts_valid = false;    // gcounts hold the global counts of the last collective sync
   bool have_pending_ug = false;  // last step did not read U_g back to the host
   int fused_last = 0;  // last step used the fused NVLS S5+S6 kernel (2: direct into E windows)
+  int last_path = PATH_NONE;
+  bool last_path_local = false;  // local-slot M layout (U_i rows written by S4)
+  bool last_peer_s3 = false;     // ids exchanged as presence bitmaps
+  bool last_table = false;       // the last step updated a table
+  cudaStream_t last_stream = nullptr;
   // CUDA graph of lmscale_step (LMSCALE_FLAG_GRAPH)
   bool capturing = false;
   cudaStream_t s_cap = nullptr;
@@ -117,6 +133,11 @@ struct lmscale_ctx {
     float lr;
     int kernels;
     int fused;
+    int path;
+    float cF;
+    int cbf;
+    bool clean_in;   // the graph's S1 assumes a zero presence bitmap on entry
+    bool clean_out;  // ... and leaves it zero
   } gkey{};
   lmscale_stats stats{};
   int kernels_call = 0;
@@ -194,57 +215,42 @@ void end_call(lmscale_ctx* c) {
   c->stats.kernels_total_lo = (int32_t)(c->kernels_total & 0x7fffffff);
 }
 
-// S1 on stream s: one launch (radix sort + run flags): a thread-
-// block cluster for K <= 64K, else a persistent grid with in-kernel barriers.
+// S1 on stream s: one launch (counting-sort grouping over the
+// vocabulary, group.cu).  world1: I = J, so it also writes I^, l2g and U_g.
 lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t* nu_out,
                       cudaStream_t s, bool world1 = false) {
-  S1Args a;
-  a.ihat = world1 ? ctx->ihat : nullptr;
-  a.l2g = world1 ? ctx->l2g : nullptr;
-  a.sc3 = world1 ? ctx->sc3 : nullptr;
+  G1Args a;
   a.ids = ids;
   a.K = (int)k;
   a.vocab = (uint32_t)ctx->cfg.vocab;
-  a.passes = ctx->plan.passes;
-  a.bits = ctx->plan.bits;
-  a.ka = ctx->keys_a;
-  a.kb = ctx->keys_b;
-  a.va = ctx->vals_a;
-  a.vb = ctx->vals_b;
-  a.cT = ctx->cT;
-  a.bT = ctx->bT;
-  a.rtot = ctx->ctot;
-  a.ntiles = (int)((k + CO_TILE - 1) / CO_TILE);
-  a.ntp = (a.ntiles + 3) / 4 * 4;
-  a.luniq = ctx->luniq;
-  a.lstart = ctx->lstart;
-  a.segidx = ctx->segidx;
-  a.inverse = ctx->inverse;
+  a.wcount = ctx->wcount;
+  a.tick = ctx->tick;
   a.lbits = ctx->lbits;
   a.lrank = ctx->lrank;
   a.W = ctx->W;
-  a.heads = ctx->heads;
+  a.ctot = ctx->ctot1;
+  a.luniq = ctx->luniq;
+  a.counts = ctx->counts;
+  a.lstart = ctx->lstart;
+  a.perm = ctx->perm;
+  a.inverse = ctx->inverse;
+  a.runfirst = ctx->runfirst;
+  a.nr = seg_ranges(k, ctx->cfg.dim, ctx->num_sms, &a.seg_len);
   a.sc = ctx->sc1;
   a.nu_out = nu_out;
+  a.zero_bits = ctx->lbits_clean ? 0 : 1;
   a.trace = ctx->trace;
+  a.ihat = world1 ? ctx->ihat : nullptr;
+  a.l2g = world1 ? ctx->l2g : nullptr;
+  a.sc3 = world1 ? ctx->sc3 : nullptr;
   a.bar = ctx->bars + 1;
-  if (!getenv("LMSCALE_NO_CLUSTER") && cluster_s1_ok((int)k)) {
-    // small K: the whole sort in one thread-block cluster (DSMEM)
-    a.passes = ctx->cl_plan.passes;
-    a.bits = ctx->cl_plan.bits;
-    CK(launch_s1_cluster(a, s));
-    LAUNCHED(1);
-    ctx->sorted_keys = nullptr;
-    ctx->sorted_vals = ctx->vals_a;
-  } else {
-    CK(launch_s1(a, ctx->num_sms, s));
-    LAUNCHED(1);
-    ctx->sorted_keys = (a.passes & 1) ? ctx->keys_a : ctx->keys_b;
-    ctx->sorted_vals = (a.passes & 1) ? ctx->vals_a : ctx->vals_b;
-  }
+  CK(launch_group(a, ctx->num_sms, s));
+  LAUNCHED(1);
+  ctx->lbits_clean = false;
   ctx->last_k = k;
   ctx->have_s1 = true;
   ctx->have_s3 = world1;
+  ctx->gcounts_valid = false;
   if (world1) ctx->last_n = k;
   return LMSCALE_OK;
 }
@@ -294,79 +300,61 @@ void print_trace(lmscale_ctx* ctx, cudaStream_t s) {
   for (int i = 33; i <= 41; ++i)
     if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
   if (t[32] > t[0]) fprintf(stderr, " | S1start->S3start %.2f us", (t[32] - t[0]) * 1e-3);
-  if (t[54])
+  if (t[54] && t[58]) {
+    const unsigned long long s0 = ~t[54];
     fprintf(stderr,
-            " | S4 cta0: phase1 %.2f (last cta done %.2f) barrier %.2f fixup %.2f (last %.2f)"
-            " | S1 end->S4 start %.2f",
-            (t[55] - t[54]) * 1e-3, (t[59] - t[54]) * 1e-3, (t[56] - t[55]) * 1e-3,
-            (t[57] - t[56]) * 1e-3, (t[61] - t[56]) * 1e-3, (t[54] - t[22]) * 1e-3);
-  if (t[62] && t[63])
-    fprintf(stderr, " | S1 cta0 last stamp -> S1 last exit %.2f, S1 last exit -> S4 first start %.2f",
-            (t[62] - t[22]) * 1e-3, ((long long)(~t[63]) - (long long)t[62]) * 1e-3);
+            " | S4 (from first CTA start): last CTA start %.2f, last prologue end %.2f,"
+            " first consumer end %.2f, last consumer end %.2f; S1 stamp0 -> S4 first start %.2f",
+            (t[55] - s0) * 1e-3, (t[56] - s0) * 1e-3, ((~t[57]) - s0) * 1e-3, (t[58] - s0) * 1e-3,
+            ((long long)s0 - (long long)t[0]) * 1e-3);
+  }
   fprintf(stderr, "\n");
 }
 
-ScatterArgs scatter_args(lmscale_ctx* ctx, const float* grad) {
-  ScatterArgs a;
-  a.grad = grad;
-  a.perm = ctx->sorted_vals;
-  a.segidx = ctx->segidx;
-  a.l2g = ctx->l2g;
-  a.lstart = ctx->lstart;
-  a.ihat = ctx->ihat;
-  a.lbits = ctx->lbits;
-  a.sc3 = ctx->sc3;
-  a.sc1 = ctx->sc1;
-  a.M = ctx->M;
-  a.partial = ctx->partial;
-  a.sc1w = ctx->sc1;
-  a.fixent = ctx->fixent;
-  a.part2 = ctx->part2;
-  a.fix_cap = (int)(2 * ctx->nchunks);
-  static const bool fx_barrier = getenv("LMSCALE_S4_FIXUP_BARRIER") != nullptr;
-  a.fx_last = fx_barrier ? 0 : 1;
-  static const int fxp = getenv("LMSCALE_S4_FXP") ? atoi(getenv("LMSCALE_S4_FXP")) : 32;
-  a.fxp = fxp > 0 ? fxp : 32;
-  a.pdl = 0;
-  a.fxcnt = ctx->fxcnt;
-  a.fx_stride = ctx->fx_stride;
-  a.zero_rows = ctx->cfg.world > 1 ? 1 : 0;  // world 1: slot = local index
-  a.fill_absent = 1;
-  a.m16 = 0;
-  a.cF = 0.f;
-  a.cbf = 0;
-  a.apply = 0;
-  a.short_runs = ctx->last_k >= (1 << 16) ? 1 : 0;
-  a.table = nullptr;
-  a.lr = 0.f;
-  a.trace = ctx->trace;
-  a.bar = ctx->bars + 0;
-  a.K = (int)ctx->last_k;
-  a.D = (int)ctx->cfg.dim;
-  a.ug_cap = std::min<int64_t>(ctx->last_n, ctx->cfg.vocab);
-  a.num_sms = ctx->num_sms;
-  return a;
-}
-
-// S4 (+ the world-1 S6 when apply): one launch.
+// S4 (+ the world-1 S6 when apply): one launch (segsum.cu).  Output slots:
+// local (slot = u: world 1, or the local-slot layout) or global (l2g, with
+// the absent slots zero-filled when fill_absent).
 lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
                       float* table = nullptr, float lr = 0.f, bool fill_absent = true,
-                      float m16_F = 0.f, bool apply = false, bool local_slots = false) {
-  ScatterArgs a = scatter_args(ctx, grad);
-  if (local_slots) a.zero_rows = 0;  // row u of M for the u-th local word
+                      float m16_F = 0.f, bool apply = false, bool local_slots = false,
+                      bool pdl = false) {
+  const bool world1 = ctx->cfg.world == 1;
+  SegArgs a{};
+  a.grad = grad;
+  a.perm = ctx->perm;
+  a.runfirst = ctx->runfirst;
+  a.lstart = ctx->lstart;
+  a.word = ctx->ihat;  // world 1: I^ = J^
+  a.l2g = (world1 || local_slots) ? nullptr : ctx->l2g;
+  a.sc1 = ctx->sc1;
   a.table = table;
   a.lr = lr;
   a.apply = apply ? 1 : 0;
-  // world 1: S4 directly follows the cluster S1 on the same stream -- launch
-  // it as a programmatic dependent (its launch overlaps S1's tail)
-  static const bool no_pdl = getenv("LMSCALE_NO_PDL") != nullptr;
-  a.pdl = (apply && !no_pdl && ctx->sorted_keys == nullptr) ? 1 : 0;
-  a.fill_absent = fill_absent ? 1 : 0;
+  a.M = ctx->M;
   a.m16 = m16_F > 0.f ? 1 : 0;
   a.cF = m16_F;
   a.cbf = ctx->cbf;
-  CK(launch_scatter(a, s));
+  a.part = ctx->part;
+  a.part2 = ctx->part2;
+  a.cnt = ctx->pcnt;
+  a.cnt2 = ctx->pcnt + 2 * (size_t)ctx->nr_max * ((ctx->cfg.dim + 511) / 512);
+  a.lbits = ctx->lbits;
+  a.W = ctx->W;
+  a.clear_bits = world1 ? 1 : 0;  // nothing reads the bitmap after S1 at world 1
+  static const bool no_pdl = getenv("LMSCALE_NO_PDL") != nullptr;
+  a.pdl = (pdl && !no_pdl) ? 1 : 0;
+  a.K = (int)ctx->last_k;
+  a.D = (int)ctx->cfg.dim;
+  a.num_sms = ctx->num_sms;
+  a.trace = ctx->trace;
+  CK(launch_seg(a, s));
   LAUNCHED(1);
+  if (world1) ctx->lbits_clean = true;
+  if (!world1 && !local_slots && fill_absent && !a.m16) {
+    CK(launch_zero_absent(ctx->M, (int)ctx->cfg.dim, ctx->ihat, ctx->lbits, ctx->sc3, ctx->sc1,
+                          std::min<int64_t>(ctx->last_n, ctx->cfg.vocab), ctx->num_sms, s));
+    LAUNCHED(1);
+  }
   rec(ctx, EV_SCATTER_END, s);
   return LMSCALE_OK;
 }
@@ -457,6 +445,13 @@ lmscale_status lmscale_set_compression(lmscale_ctx* ctx, float F) {
                 ctx->nvls_why);
   if (F > 0.f && (ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
     return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "compression on a NO_COMM context");
+  if (F > 0.f && ctx->cfg.world > 8)
+    return fail(ctx, LMSCALE_ERR_UNSUPPORTED,
+                "the compressed exchange addresses at most 8 peers (world %d)", ctx->cfg.world);
+  if (F != ctx->cF && ctx->gexec) {  // a captured step carries the old F
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
   ctx->cF = F;
   return LMSCALE_OK;
 }
@@ -563,11 +558,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->W = (cfg->vocab + 31) / 32;
     ctx->NI = (int64_t)cfg->world * cfg->max_tokens;
     ctx->ucap = std::min<int64_t>(ctx->NI, cfg->vocab);
-    ctx->nchunks = (ctx->K + SC_CHUNK - 1) / SC_CHUNK;
-    ctx->ntiles_max = (ctx->K + CO_TILE - 1) / CO_TILE;
-    ctx->ntp_max = (ctx->ntiles_max + 3) / 4 * 4;
-    ctx->plan = make_coop_plan((uint64_t)cfg->vocab);
-    ctx->cl_plan = make_cluster_plan((uint64_t)cfg->vocab);
+    ctx->nr_max = seg_max_ranges(ctx->K, ctx->num_sms);
     const int64_t K = ctx->K, D = cfg->dim;
     // ---- workspace layout (one allocation, 256-byte aligned sub-buffers)
     size_t off = 0;
@@ -576,16 +567,14 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       off = align_up(off + bytes);
       return o;
     };
-    size_t o_keys_a = take(4 * K), o_keys_b = take(4 * K), o_vals_a = take(4 * K),
-           o_vals_b = take(4 * K), o_segidx = take(4 * K), o_inverse = take(4 * K),
-           o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)), o_counts = take(4 * K),
-           o_l2g = take(4 * K), o_wrank = take(4 * ctx->W), o_I = take(4 * ctx->NI),
-           o_ihat = take(4 * ctx->ucap), o_fix = take(8 * 2 * ctx->nchunks),
-           o_bars = take(sizeof(GridBar) * 8);
+    size_t o_perm = take(4 * K), o_tick = take(4 * K),
+           o_inverse = take(4 * K), o_luniq = take(4 * K), o_lstart = take(4 * (K + 1)),
+           o_counts = take(4 * K), o_l2g = take(4 * K), o_wrank = take(4 * ctx->W),
+           o_I = take(4 * ctx->NI), o_ihat = take(4 * ctx->ucap),
+           o_gcounts = take(4 * ctx->ucap), o_bars = take(sizeof(GridBar) * 8),
+           o_wcount = take(4 * 32 * (size_t)ctx->W), o_lrank = take(4 * ctx->W);
     size_t o_sc3 = take(sizeof(Sc3) + sizeof(Sc1)), o_sc1 = o_sc3 + sizeof(Sc3),
-           o_cT = take(4 * (size_t)ctx->plan.passes * (1u << ctx->plan.bits) * ctx->ntp_max),
-           o_heads = take(4 * ctx->ntiles_max), o_ctot = take(4 * 4096),
-           o_bT = take(4 * (size_t)ctx->ntiles_max * (1u << ctx->plan.bits)),
+           o_ctot = take(4 * 4096), o_ctot1 = take(4 * 2 * (size_t)G1_STRIPES * G1_MAX_GRID),
            o_lbits = take(4 * ctx->W), o_gbits = take(4 * ctx->W), o_epoch = take(64),
            o_ck = take(16 * (size_t)(cfg->world + 1));
     // M lives in its own allocation: with a communicator it comes from
@@ -593,21 +582,18 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     // (+256: room to align the compressed M^ region at byte 2*ucap*D)
     const size_t m_bytes = align_up(4 * (size_t)ctx->ucap * D + 256, 1 << 21);
     ctx->mhat_off = align_up(2 * (size_t)ctx->ucap * D, 256);
-    size_t o_part = take(4 * (size_t)2 * ctx->nchunks * D);
-    size_t o_part2 = take(4 * (size_t)2 * ctx->nchunks * D);
-    ctx->fx_stride = 2 * ctx->nchunks * ((D + 127) / 128 + 1);
-    size_t o_fxcnt = take(4 * 2 * (size_t)ctx->fx_stride);
+    size_t o_part = take(4 * (size_t)2 * ctx->nr_max * D);
+    size_t o_part2 = take(4 * (size_t)2 * ctx->nr_max * D);
+    size_t o_pcnt = take(4 * (size_t)3 * ctx->nr_max * ((D + 511) / 512));
+    size_t o_runfirst = take(4 * ((size_t)ctx->nr_max + 1));
     ctx->ws_bytes = off;
     if (cudaMalloc(&ctx->base, off) != cudaSuccess) {
       cudaGetLastError();
       return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(%zu) failed", off);
     }
     char* b = (char*)ctx->base;
-    ctx->keys_a = (uint32_t*)(b + o_keys_a);
-    ctx->keys_b = (uint32_t*)(b + o_keys_b);
-    ctx->vals_a = (int32_t*)(b + o_vals_a);
-    ctx->vals_b = (int32_t*)(b + o_vals_b);
-    ctx->segidx = (int32_t*)(b + o_segidx);
+    ctx->perm = (int32_t*)(b + o_perm);
+    ctx->tick = (uint32_t*)(b + o_tick);
     ctx->inverse = (int32_t*)(b + o_inverse);
     ctx->luniq = (uint32_t*)(b + o_luniq);
     ctx->lstart = (int32_t*)(b + o_lstart);
@@ -616,21 +602,22 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->wrank = (uint32_t*)(b + o_wrank);
     ctx->I = (uint32_t*)(b + o_I);
     ctx->ihat = (uint32_t*)(b + o_ihat);
-    ctx->fixent = (int2*)(b + o_fix);
+    ctx->gcounts = (int32_t*)(b + o_gcounts);
     ctx->bars = (GridBar*)(b + o_bars);
+    ctx->wcount = (uint32_t*)(b + o_wcount);
+    ctx->lrank = (uint32_t*)(b + o_lrank);  // moves into the window when there is one
     ctx->sc1 = (Sc1*)(b + o_sc1);
     ctx->sc3 = (Sc3*)(b + o_sc3);
-    ctx->cT = (uint32_t*)(b + o_cT);
-    ctx->heads = (uint32_t*)(b + o_heads);
-    ctx->bT = (uint32_t*)(b + o_bT);
     ctx->ctot = (uint32_t*)(b + o_ctot);
+    ctx->ctot1 = (uint32_t*)(b + o_ctot1);
     ctx->lbits = (uint32_t*)(b + o_lbits);
     ctx->gbits = (uint32_t*)(b + o_gbits);
     ctx->s3_epoch = (uint32_t*)(b + o_epoch);
     ctx->ck_dev = (void*)(b + o_ck);
-    ctx->partial = (float*)(b + o_part);
+    ctx->part = (float*)(b + o_part);
+    ctx->pcnt = (uint32_t*)(b + o_pcnt);
     ctx->part2 = (float*)(b + o_part2);
-    ctx->fxcnt = (uint32_t*)(b + o_fxcnt);
+    ctx->runfirst = (int32_t*)(b + o_runfirst);
     CK(cudaMemset(ctx->base, 0, off));
     CK(cudaHostAlloc((void**)&ctx->h_sc3, sizeof(Sc3) + sizeof(Sc1), cudaHostAllocDefault));
     ctx->h_sc1 = (Sc1*)((char*)ctx->h_sc3 + sizeof(Sc3));
@@ -654,7 +641,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
       // the fused kernel reads the peers' bitmaps to load only present rows
       const size_t lb_off = m_bytes;
       const size_t lr_off = align_up(m_bytes + 4 * (size_t)ctx->W, 256);
-      const size_t fl_off = align_up(lr_off + 4 * (size_t)ctx->W, 256);
+      const size_t ct_off = align_up(lr_off + 4 * (size_t)ctx->W, 256);
+      const size_t fl_off = align_up(ct_off + 4 * (size_t)K, 256);
       const size_t win_bytes = align_up(fl_off + 4 * 64, 1 << 21);
       void* m = nullptr;
       if (ncclMemAlloc(&m, win_bytes) != ncclSuccess)
@@ -674,6 +662,8 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
         ctx->flags_off = fl_off;
         ctx->lrank_off = lr_off;
         ctx->lrank = (uint32_t*)((char*)m + lr_off);
+        ctx->counts_off = ct_off;
+        ctx->counts = (int32_t*)((char*)m + ct_off);
         ctx->peer_s3 = !getenv("LMSCALE_NO_PEER_S3") && cfg->world <= 8 &&
                        nvls_peer_bases(ctx->nvls, cfg->world, (void**)ctx->peer_base);
       } else {
@@ -757,6 +747,8 @@ lmscale_status lmscale_unique(lmscale_ctx* ctx, const uint32_t* ids, int64_t k,
   if (st) return st;
   begin_call(ctx);
   cudaStream_t s = S(stream);
+  ctx->last_path = PATH_NONE;
+  ctx->m_consumed = false;
   st = run_s1(ctx, ids, k, num_unique_out, s);
   if (st) return st;
   if (uniq_out || counts_out || inverse_out) {
@@ -805,8 +797,10 @@ lmscale_status lmscale_get_sparse_grad(lmscale_ctx* ctx, lmscale_sparse_grad* ou
   CK(cudaMemcpy(ctx->h_sc3, ctx->sc3, sizeof(Sc3), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(ctx->h_sc1, ctx->sc1, sizeof(Sc1), cudaMemcpyDeviceToHost));
   out->ids = ctx->ihat;
-  out->rows = ctx->M;
+  out->counts = ctx->gcounts_valid ? (ctx->cfg.world == 1 ? ctx->counts : ctx->gcounts) : nullptr;
+  out->rows = ctx->m_consumed ? nullptr : ctx->M;  // S6 folded / fused S5+S6 consumed M
   out->num_unique = ctx->h_sc3->u_global;
+  ctx->have_pending_ug = false;
   ctx->stats.u_global = ctx->h_sc3->u_global;
   ctx->stats.u_local = ctx->h_sc1->u_local;
   if ((ctx->h_sc3->err | ctx->h_sc1->err) & 1u)
@@ -822,9 +816,6 @@ lmscale_status lmscale_get_local_maps(lmscale_ctx* ctx, const uint32_t** uniq,
   if (!ctx) return LMSCALE_ERR_INVALID_ARG;
   if (!ctx->have_s1) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "no S1 computed yet");
   cudaStream_t s = S(stream);
-  launch_counts_export(ctx->lstart, ctx->luniq, ctx->inverse, ctx->sc1, (int)ctx->last_k,
-                       ctx->counts, nullptr, nullptr, nullptr, s);
-  LAUNCHED(1);
   CK(cudaStreamSynchronize(s));
   CK(cudaMemcpy(ctx->h_sc1, ctx->sc1, sizeof(Sc1), cudaMemcpyDeviceToHost));
   if (uniq) *uniq = ctx->luniq;
@@ -870,14 +861,15 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   // the peer-to-peer fused kernels load only present rows: no zero-fill of M
   const bool p2p = G > 1 && table && ctx->nvls &&
                    (comp || (table == ctx->table_ptr && ctx->table_win && nvls_use_p2p(G)));
-  // local-slot layout (small K, peer S3, P2P): S4 writes row u of M_g for the
-  // u-th local word (no l2g needed), so it runs on the side stream while S3
-  // runs -- safe because this S4 variant has no grid barrier.  The fused
-  // kernel finds word w's row on rank j as lrank_j[w/32] + popc(bits below w).
+  // local-slot layout (peer S3, P2P): S4 writes row u of M_g for the u-th
+  // local word (no l2g needed), so it runs on the side stream while S3 runs
+  // (S4 has no grid barrier).  The fused kernel finds word w's row on rank j
+  // as lrank_j[w/32] + popc(bits below w).
   static const bool no_local = getenv("LMSCALE_NO_S4_OVERLAP") != nullptr;
-  static const bool fx_barrier = getenv("LMSCALE_S4_FIXUP_BARRIER") != nullptr;
-  const bool local_m = peer_s3 && p2p && ctx->lrank && k < (1 << 16) && !fx_barrier && !no_local;
+  const bool local_m = peer_s3 && p2p && !no_local;
   const bool overlap = local_m && ctx->tmode == 0;  // timed passes measure S4 alone
+  ctx->m_consumed = false;
+  ctx->gcounts_valid = false;
   if (peer_s3) {
     // J^-set exchange: no ID all-gather; S3 ORs the G
     // local presence bitmaps over NVLink after S1 (same I^, U_g and l2g).
@@ -950,23 +942,36 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
                        ctx->s_copy));
     CK(cudaEventRecord(ctx->ev_copy, ctx->s_copy));
   }
-  // S4: segmented scatter-add into M; with one rank
-  // the all-reduce is the identity and S6 rides in the same launch.
-  // (fusing S6 into S4's cooperative kernel at world 1 was measured slower
-  // than the separate, higher-occupancy update launch; kept separate)
-  const bool fuse_s6 = false;
-  // world 1: S6 folded into S4 (finished rows go straight into the table; M
-  // is not written and not re-read).  LMSCALE_NO_INLINE_S6: separate k_update.
+  // global counts of I^ for the borrowed view of lmscale_sync_embedding_grad
+  // (world 1: S1's counts are already the global ones)
+  const bool want_counts = out && !table;
+  if (want_counts && G > 1) {
+    CK(launch_gcounts(ctx->gcounts, ctx->ucap, ctx->ihat, ctx->sc3, peer_s3 ? nullptr : I, n,
+                      ctx->gbits, ctx->wrank, (uint32_t)ctx->cfg.vocab, G,
+                      peer_s3 ? ctx->peer_base : nullptr, ctx->lbits_off, ctx->lrank_off,
+                      ctx->counts_off, ctx->num_sms, s));
+    LAUNCHED(1);
+    ctx->gcounts_valid = true;
+  }
+  // S4: segmented scatter-add into M.  World 1: S6
+  // folded in (finished rows go straight into the table; M is not written
+  // and not re-read).  LMSCALE_NO_INLINE_S6: separate k_update.
   static const bool no_inline = getenv("LMSCALE_NO_INLINE_S6") != nullptr;
   const bool inline_s6 = G == 1 && table && !no_inline;
   if (overlap) {
     CK(cudaStreamWaitEvent(s, ctx->ev_s4, 0));  // S4 ran beside S3
   } else {
-    st = run_s4(ctx, grad, s, (fuse_s6 || inline_s6) ? table : nullptr, lr,
-                /*fill_absent=*/G > 1 && !p2p, comp ? ctx->cF : 0.f, inline_s6, local_m);
+    st = run_s4(ctx, grad, s, inline_s6 ? table : nullptr, lr, /*fill_absent=*/G > 1 && !p2p,
+                comp ? ctx->cF : 0.f, inline_s6, local_m, /*pdl=*/G == 1);
     if (st) return st;
   }
   rec(ctx, EV_FIXUP_END, s);
+  ctx->last_path = G == 1 ? (inline_s6 ? PATH_W1_FOLD : (table ? PATH_W1_UPDATE : PATH_W1_SYNC))
+                          : PATH_NCCL;
+  ctx->last_path_local = local_m;
+  ctx->last_peer_s3 = peer_s3;
+  ctx->last_table = table != nullptr;
+  ctx->last_stream = s;
   if (G > 1 && table && ctx->nvls) {
     // S5+S6 fused over NVLS: no host round trip, U_g is read on the device.
     launch_nvls_update(ctx->nvls, ctx->ihat, ctx->sc3, table, ctx->M, (int)D, lr,
@@ -991,9 +996,13 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
     ctx->fused_last = comp ? 3 : (table == ctx->table_ptr && ctx->table_win) ? 2 : 1;
+    ctx->last_path = comp ? PATH_P2P_COMP : ctx->fused_last == 2 ? PATH_P2P : PATH_NVLS;
+    ctx->m_consumed = true;
+    ctx->have_pending_ug = true;
     int64_t ug = -1;
     if (need_host_ug) {
       CK(cudaEventSynchronize(ctx->ev_copy));
+      ctx->have_pending_ug = false;
       ug = ctx->h_sc3->u_global;
       ctx->stats.u_global = ug;
       ctx->stats.u_local = ctx->h_sc1->u_local;
@@ -1005,6 +1014,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     }
     if (out) {
       out->ids = ctx->ihat;
+      out->counts = nullptr;
       out->rows = nullptr;  // M was consumed by the fused update
       out->num_unique = ug;
     }
@@ -1024,9 +1034,11 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     ctx->update_timed = timing(ctx);
     ctx->timing_valid = timing(ctx);
     ctx->have_pending_ug = true;
+    ctx->m_consumed = inline_s6;
     print_trace(ctx, s);
     if (out) {
       out->ids = ctx->ihat;
+      out->counts = nullptr;
       out->rows = inline_s6 ? nullptr : ctx->M;  // folded S6 consumed the rows
       out->num_unique = -1;
     }
@@ -1051,24 +1063,23 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   rec(ctx, EV_AR_END, s);
   if (table) {
     rec(ctx, EV_UPD_BEGIN, s);
-    if (!fuse_s6 && !inline_s6) {
+    if (!inline_s6) {
       launch_update(table, (int)D, ctx->ihat, ctx->M, ug, nullptr, lr, ctx->num_sms, s);
       if (ug > 0) LAUNCHED(1);
     }
     rec(ctx, EV_UPD_END, s);
     ctx->update_timed = timing(ctx);
   }
+  ctx->m_consumed = inline_s6;
   print_trace(ctx, s);
 
   if (out) {
     out->ids = ctx->ihat;
+    out->counts = want_counts ? (G == 1 ? ctx->counts : ctx->gcounts) : nullptr;
     out->rows = inline_s6 ? nullptr : ctx->M;
     out->num_unique = ug;
   }
-  ctx->stats.bytes_ids_gathered = 4 * (int64_t)(G - 1) * k;
-  ctx->stats.bytes_grad_allreduce = G > 1 ? 4 * ug * D : 0;
-  ctx->stats.bytes_scatter = 4 * k * D + 4 * ug * D;
-  ctx->stats.bytes_update = 12 * ug * D;
+  if (want_counts && G == 1) ctx->gcounts_valid = true;
   ctx->timing_valid = timing(ctx);
   end_call(ctx);
   return LMSCALE_OK;
@@ -1099,7 +1110,8 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
     if (st0) return st0;
     cudaStream_t s = S(stream);
     const bool hit = ctx->gexec && ctx->gkey.ids == ids && ctx->gkey.grad == grad &&
-                     ctx->gkey.table == table && ctx->gkey.k == k && ctx->gkey.lr == lr;
+                     ctx->gkey.table == table && ctx->gkey.k == k && ctx->gkey.lr == lr &&
+                     ctx->gkey.cF == ctx->cF && ctx->gkey.cbf == ctx->cbf;
     if (!hit) {
       if (ctx->gexec) {
         cudaGraphExecDestroy(ctx->gexec);
@@ -1107,6 +1119,12 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
       }
       // capture on the library's own stream (the caller's may be the legacy
       // default stream, which cannot be captured)
+      if (ctx->cfg.world == 1 && !ctx->lbits_clean) {
+        // world 1 leaves the bitmap clean: capture the S1 that relies on it
+        CK(cudaMemsetAsync(ctx->lbits, 0, 4 * (size_t)ctx->W, s));
+        ctx->lbits_clean = true;
+      }
+      const bool clean_in = ctx->lbits_clean;
       CK(cudaStreamBeginCapture(ctx->s_cap, cudaStreamCaptureModeThreadLocal));
       ctx->capturing = true;
       lmscale_sparse_grad sg;
@@ -1114,6 +1132,8 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
       ctx->capturing = false;
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(ctx->s_cap, &g);
+      const bool clean_out = ctx->lbits_clean;
+      ctx->lbits_clean = clean_in;  // nothing ran yet
       if (st) {
         if (g) cudaGraphDestroy(g);
         return st;
@@ -1131,16 +1151,31 @@ lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* 
       ctx->gkey.table = table;
       ctx->gkey.k = k;
       ctx->gkey.lr = lr;
+      ctx->gkey.cF = ctx->cF;
+      ctx->gkey.cbf = ctx->cbf;
       ctx->gkey.kernels = ctx->kernels_call;
       ctx->gkey.fused = ctx->fused_last;
+      ctx->gkey.path = ctx->last_path;
+      ctx->gkey.clean_in = clean_in;
+      ctx->gkey.clean_out = clean_out;
       ctx->kernels_total -= ctx->kernels_call;  // captured, not launched yet
     }
+    // the graph's S1 skips clearing the presence bitmap when it was captured
+    // with a clean one: restore that precondition if a staged call dirtied it
+    if (ctx->gkey.clean_in && !ctx->lbits_clean)
+      CK(cudaMemsetAsync(ctx->lbits, 0, 4 * (size_t)ctx->W, s));
     begin_call(ctx);
     if (ctx->trace) CK(cudaMemsetAsync(ctx->trace, 0, 64 * sizeof(unsigned long long), s));
     CK(cudaGraphLaunch(ctx->gexec, s));
     print_trace(ctx, s);
     ctx->kernels_call = ctx->gkey.kernels;
     ctx->fused_last = ctx->gkey.fused;
+    ctx->last_path = ctx->gkey.path;
+    ctx->lbits_clean = ctx->gkey.clean_out;
+    ctx->last_stream = s;
+    ctx->have_pending_ug = true;
+    ctx->m_consumed = ctx->fused_last != 0 || ctx->last_path == PATH_W1_FOLD;
+    ctx->gcounts_valid = false;
     ctx->timing_valid = timing(ctx);
     ctx->update_timed = timing(ctx);
     ctx->have_s1 = ctx->have_s3 = true;
@@ -1272,6 +1307,28 @@ lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
     st.us_allreduce = 1e3 * ev_ms(ctx, EV_FIXUP_END, EV_AR_END);
     st.us_update = ctx->update_timed ? 1e3 * ev_ms(ctx, EV_UPD_BEGIN, EV_UPD_END) : -1.0;
     st.us_total = 1e3 * ev_ms(ctx, EV_FORK, ctx->update_timed ? EV_UPD_END : EV_AR_END);
+  }
+  // byte accounting of the last step (SURVEY 8(d) algorithmic bytes, per rank),
+  // for the kernels that actually ran; U_g / U_i read back if the step kept
+  // them on the device
+  if (ctx->last_path != PATH_NONE) {
+    if (ctx->have_pending_ug && !ctx->capturing) {
+      CK(cudaStreamSynchronize(ctx->last_stream));
+      CK(cudaMemcpy(ctx->h_sc3, ctx->sc3, sizeof(Sc3) + sizeof(Sc1), cudaMemcpyDeviceToHost));
+      ctx->have_pending_ug = false;
+      st.u_global = ctx->h_sc3->u_global;
+      st.u_local = ctx->h_sc1->u_local;
+    }
+    const int64_t G = ctx->cfg.world, D = ctx->cfg.dim, k = ctx->last_k;
+    const int64_t ug = st.u_global, ui = st.u_local;
+    const int p = ctx->last_path;
+    const int64_t esz = p == PATH_P2P_COMP ? 2 : 4;
+    st.bytes_ids_gathered = G == 1 ? 0 : ctx->last_peer_s3 ? 4 * ctx->W * (G - 1) : 4 * (G - 1) * k;
+    st.bytes_grad_allreduce = G == 1 ? 0 : esz * ug * D;
+    st.bytes_scatter = 4 * k * D + (p == PATH_W1_FOLD ? 8 * ug * D
+                                    : ctx->last_path_local ? esz * ui * D : esz * ug * D);
+    st.bytes_update =
+        (p == PATH_W1_UPDATE || (p == PATH_NCCL && ctx->last_table)) ? 12 * ug * D : 0;
   }
   st.fused_s5_s6 = ctx->fused_last;
   st.nvls_available = ctx->nvls ? 1 : 0;

@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
                                          /*multimem=*/true);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  // an id >= vocab on any rank (S3's error bit is the OR over ranks): every
+  // rank leaves here, no table row is touched (lmscale_sync semantics)
+  if (__ldcg(&a.sc3->err) & 1u) return;
   nv_stamp(a.trace, 49);
 
   const int64_t Ug = a.sc3->u_global;
@@ -204,6 +207,9 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
                                          /*multimem=*/true);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  // an id >= vocab on any rank (S3's error bit is the OR over ranks): every
+  // rank leaves here, no table row is touched (lmscale_sync semantics)
+  if (__ldcg(&a.sc3->err) & 1u) return;
   const int64_t Ug = a.sc3->u_global;
   const int C = a.D / W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -300,6 +306,9 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
                                          /*multimem=*/true);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's compressed M_g is complete
+  // an id >= vocab on any rank (S3's error bit is the OR over ranks): every
+  // rank leaves here, no table row is touched (lmscale_sync semantics)
+  if (__ldcg(&a.sc3->err) & 1u) return;
   const int64_t Ug = a.sc3->u_global;
   const int C = a.D / W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

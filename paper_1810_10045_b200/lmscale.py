@@ -39,7 +39,7 @@ class Config(ctypes.Structure):
 
 
 class SparseGradC(ctypes.Structure):
-    _fields_ = [("ids", _P), ("rows", _P), ("num_unique", _i64)]
+    _fields_ = [("ids", _P), ("counts", _P), ("rows", _P), ("num_unique", _i64)]
 
 
 class StatsC(ctypes.Structure):
@@ -172,13 +172,16 @@ def _stream(stream=None):
 
 
 class SparseGrad:
-    """I^ (uint32[U_g]) and M^ (float32[U_g, D]) as zero-copy device views."""
+    """I^ (uint32[U_g]), the global counts (int32[U_g], or None) and M^
+    (float32[U_g, D], or None when a step consumed it) as zero-copy device views."""
 
     def __init__(self, c: SparseGradC, dim: int, device):
         self.c = c
         self.num_unique = int(c.num_unique)
-        self.ids = _view(c.ids, (self.num_unique,), torch.int32, device)  # uint32 bit patterns
-        self.rows = _view(c.rows, (self.num_unique, dim), torch.float32, device)
+        n = max(self.num_unique, 0)
+        self.ids = _view(c.ids, (n,), torch.int32, device)  # uint32 bit patterns
+        self.counts = _view(c.counts, (n,), torch.int32, device) if c.counts else None
+        self.rows = _view(c.rows, (n, dim), torch.float32, device) if c.rows else None
 
     @classmethod
     def from_tensors(cls, ids: torch.Tensor, rows: torch.Tensor) -> "SparseGrad":
@@ -186,9 +189,9 @@ class SparseGrad:
         assert ids.is_cuda and rows.is_cuda and rows.is_contiguous() and ids.is_contiguous()
         assert rows.dtype == torch.float32 and ids.numel() == rows.shape[0]
         self = cls.__new__(cls)
-        self.c = SparseGradC(ids.data_ptr(), rows.data_ptr(), ids.numel())
+        self.c = SparseGradC(ids.data_ptr(), None, rows.data_ptr(), ids.numel())
         self.num_unique = ids.numel()
-        self.ids, self.rows = ids, rows
+        self.ids, self.rows, self.counts = ids, rows, None
         return self
 
 

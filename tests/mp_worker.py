@@ -148,8 +148,9 @@ def run_consistency_check(cfg, rank, G, dev):
 def run_graph_equals_eager(cfg, rank, G, dev, F=0.0):
     """World > 1 with LMSCALE_FLAG_GRAPH (peer-bitmap S3 + fused S5+S6, no NCCL
     host calls): three captured-and-replayed steps give the same table bits as
-    three eager steps, new buffer contents included."""
-    mode = "signed"
+    three eager steps, new buffer contents included.  INT mode: sums are exact
+    in any order (S1's grouping order is the tickets' arrival order, R18)."""
+    mode = "int"
     lr = synth.default_lr(mode)
     ids = torch.from_numpy(synth.ids_for(cfg, rank).view(np.int32)).to(dev)
     g = synth.grad_values(cfg.K, cfg.D, mode, rank=rank).to(dev)
