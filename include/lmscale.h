@@ -271,7 +271,9 @@ LMSCALE_API lmscale_status lmscale_alloc_table(lmscale_ctx* ctx, float** table_o
 /* Timing mode of subsequent calls: 0 none, 1 only the two events bracketing
  * the S4 kernel (us_scatter), 2 every phase (all us_* fields; each event is a
  * GPU-side serialisation point of a few microseconds, so mode 2 inflates the
- * step it measures).  FLAG_TIMING at init selects mode 2. */
+ * step it measures), 3 only the two events bracketing the S5 (+ S6) phase
+ * (us_allreduce: the fused S5+S6 kernel at world > 1).  FLAG_TIMING at init
+ * selects mode 2.  INVALID_ARG outside 0..3. */
 LMSCALE_API lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode);
 
 /* Compression (Sec. 3.3; reading R15).  F > 0 makes

@@ -58,6 +58,8 @@ def _load():
             lib.oracle_unique_local.argtypes = [P, i64, P, P, P]
             lib.oracle_reduce_local.restype = None
             lib.oracle_reduce_local.argtypes = [P, i64, i64, P, i64, P]
+            lib.oracle_reduce_local_cols.restype = None
+            lib.oracle_reduce_local_cols.argtypes = [P, i64, i64, P, i64, P, i64, i64]
             lib.oracle_allgather_ids.restype = None
             lib.oracle_allgather_ids.argtypes = [P, P, ctypes.c_int, P]
             lib.oracle_unique_global.restype = i64
@@ -141,6 +143,25 @@ def reduce_local(delta, inverse, U):
     return out
 
 
+def reduce_local_threads(delta, inverse, U, threads):
+    """Step 2 split over ``threads`` column blocks run concurrently (ctypes
+    releases the GIL): bit-identical to ``reduce_local`` (same loop, same
+    per-element order).  bench.py's all-cores cpu_baseline only."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib = _load()
+    delta = _f32(delta)
+    K, D = delta.shape
+    inverse = np.ascontiguousarray(inverse, dtype=np.int32)
+    out = np.empty((U, D), np.float64)
+    nt = max(1, min(int(threads), D))
+    cuts = [D * t // nt for t in range(nt + 1)]
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(lambda t: lib.oracle_reduce_local_cols(_p(delta), K, D, _p(inverse), U,
+                                                           _p(out), cuts[t], cuts[t + 1]),
+                    range(nt)))
+    return out
+
+
 def allgather_ids(J_list):
     """Step 3. Rank-ordered concatenation I of every rank's J."""
     lib = _load()
@@ -219,6 +240,29 @@ def sync_unique(J_list, delta_list, E, lr):
     for g in range(G):                                   # steps 1, 2
         Jhat, counts, inverse = unique_local(J_list[g])
         dhat = reduce_local(delta_list[g], inverse, Jhat.size)
+        ranks.append(dict(Jhat=Jhat, counts=counts, inverse=inverse, dhat=dhat))
+    I = allgather_ids(J_list)                            # step 3
+    Ihat, gcounts = unique_global(I)                     # step 4
+    Ug = Ihat.size
+    Ms = []
+    for r in ranks:
+        r["l2g"], r["slot"] = remap(r["Jhat"], Ihat, r["inverse"])
+        Ms.append(scatter_expand(r["dhat"], r["l2g"], Ug))   # step 5
+    Mhat64 = allreduce_sum(Ms)                           # step 6
+    update_rows(E, Ihat, Mhat64, lr)                     # step 7
+    return dict(ranks=ranks, I=I, Ihat=Ihat, Ug=Ug, gcounts=gcounts, M=Ms,
+                Mhat64=Mhat64, Mhat=Mhat64.astype(np.float32), E=E)
+
+
+def sync_unique_threads(J_list, delta_list, E, lr, threads):
+    """``sync_unique`` with step 2 (the Theta(KD) local reduction, the bulk of
+    the work) split over ``threads`` column blocks: the same seven steps in
+    the same order, bit-identical results (bench.py's all-cores cpu_baseline)."""
+    G = len(J_list)
+    ranks = []
+    for g in range(G):                                   # steps 1, 2
+        Jhat, counts, inverse = unique_local(J_list[g])
+        dhat = reduce_local_threads(delta_list[g], inverse, Jhat.size, threads)
         ranks.append(dict(Jhat=Jhat, counts=counts, inverse=inverse, dhat=dhat))
     I = allgather_ids(J_list)                            # step 3
     Ihat, gcounts = unique_global(I)                     # step 4

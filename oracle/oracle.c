@@ -80,6 +80,24 @@ void oracle_reduce_local(const float* delta, int64_t K, int64_t D,
 }
 
 /*
+ * Step 2 restricted to the columns [c0, c1) of every row: the same loop (same
+ * per-element summation order, ascending p), so any split of the columns
+ * gives bit-identical results.  Used only by the all-cores timing variant of
+ * bench.py's cpu_baseline (one thread per column block).
+ */
+void oracle_reduce_local_cols(const float* delta, int64_t K, int64_t D,
+                              const int32_t* inverse, int64_t U, double* dhat, int64_t c0,
+                              int64_t c1) {
+  for (int64_t r = 0; r < U; ++r)
+    for (int64_t d = c0; d < c1; ++d) dhat[r * D + d] = 0.0;
+  for (int64_t p = 0; p < K; ++p) {
+    double* row = dhat + (int64_t)inverse[p] * D;
+    const float* src = delta + p * D;
+    for (int64_t d = c0; d < c1; ++d) row[d] += (double)src[d];
+  }
+}
+
+/*
  * Step 3: AllGather over the J vectors of all G GPUs; I is their
  * rank-ordered concatenation (reading R1: the text's J, not J^).
  * Simulated here by copying rank g's K_g ids to offset sum_{h<g} K_h.

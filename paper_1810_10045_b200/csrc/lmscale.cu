@@ -45,6 +45,9 @@ enum Ev {
   EV_COUNT
 };
 
+// pieces of the dense baseline's all-gather (each scattered on arrival)
+constexpr int DENSE_CHUNKS = 4;
+
 // which kernels the last step ran (for lmscale_get_stats' byte accounting)
 enum PathKind {
   PATH_NONE = 0,
@@ -104,6 +107,7 @@ struct lmscale_ctx {
   Sc3* sc3;
   // lazily allocated
   float* grad_all = nullptr;
+  cudaEvent_t ev_dense[DENSE_CHUNKS] = {};
   uint32_t* stage_ids = nullptr;
   float* stage_grad = nullptr;
   // pinned host mirror of {Sc3, Sc1}
@@ -199,6 +203,7 @@ bool timing(const lmscale_ctx* c) { return c->tmode != 0; }
 void rec(lmscale_ctx* c, int ev, cudaStream_t s) {
   if (c->tmode == 0) return;
   if (c->tmode == 1 && ev != EV_S3_END && ev != EV_SCATTER_END) return;
+  if (c->tmode == 3 && ev != EV_FIXUP_END && ev != EV_AR_END) return;
   if (c->capturing)  // a timing node inside the CUDA graph
     cudaEventRecordWithFlags(c->tev[ev], s, cudaEventRecordExternal);
   else
@@ -520,7 +525,7 @@ lmscale_status lmscale_lookup(lmscale_ctx* ctx, const uint32_t* ids, int64_t k,
 }
 
 lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode) {
-  if (!ctx || mode < 0 || mode > 2) return LMSCALE_ERR_INVALID_ARG;
+  if (!ctx || mode < 0 || mode > 3) return LMSCALE_ERR_INVALID_ARG;
   if (mode != ctx->tmode && ctx->gexec) {  // the captured graph carries the old events
     cudaGraphExecDestroy(ctx->gexec);
     ctx->gexec = nullptr;
@@ -733,6 +738,8 @@ void lmscale_destroy(lmscale_ctx* ctx) {
   if (ctx->base) cudaFree(ctx->base);
   if (ctx->trace) cudaFree(ctx->trace);
   if (ctx->grad_all) cudaFree(ctx->grad_all);
+  for (int c = 0; c < DENSE_CHUNKS; ++c)
+    if (ctx->ev_dense[c]) cudaEventDestroy(ctx->ev_dense[c]);
   if (ctx->stage_ids) cudaFree(ctx->stage_ids);
   if (ctx->stage_grad) cudaFree(ctx->stage_grad);
   delete ctx;
@@ -1244,13 +1251,36 @@ lmscale_status lmscale_sync_dense_baseline(lmscale_ctx* ctx, const uint32_t* ids
         return fail(ctx, LMSCALE_ERR_OOM, "dense gather buffer (%lld bytes)",
                     (long long)(4 * ctx->NI * D));
       }
+      for (int c = 0; c < DENSE_CHUNKS; ++c)
+        CK(cudaEventCreateWithFlags(&ctx->ev_dense[c], cudaEventDisableTiming));
     }
-    NK(ncclGroupStart());
-    NK(ncclAllGather(ids, ctx->I, (size_t)k, ncclUint32, ctx->comm, s));
-    NK(ncclAllGather(grad, ctx->grad_all, (size_t)(k * D), ncclFloat, ctx->comm, s));
-    NK(ncclGroupEnd());
-    I = ctx->I;
-    A = ctx->grad_all;
+    // The Theta(G K D) all-gather in DENSE_CHUNKS pieces on `s`; each piece's
+    // atomic scatter runs on the side stream as soon as the piece has arrived,
+    // overlapping the gather of the next one.
+    const int64_t kc = (k + DENSE_CHUNKS - 1) / DENSE_CHUNKS;
+    CK(cudaEventRecord(ctx->ev_fork, s));
+    CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_fork, 0));
+    int nlaunch = 0;
+    for (int c = 0; c < DENSE_CHUNKS; ++c) {
+      const int64_t r0 = c * kc, n = std::min<int64_t>(kc, k - r0);
+      if (n <= 0) break;
+      uint32_t* Ic = ctx->I + (size_t)G * r0;
+      float* Ac = ctx->grad_all + (size_t)G * r0 * D;
+      NK(ncclGroupStart());
+      NK(ncclAllGather(ids + r0, Ic, (size_t)n, ncclUint32, ctx->comm, s));
+      NK(ncclAllGather(grad + r0 * D, Ac, (size_t)(n * D), ncclFloat, ctx->comm, s));
+      NK(ncclGroupEnd());
+      CK(cudaEventRecord(ctx->ev_dense[c], s));
+      CK(cudaStreamWaitEvent(ctx->s_side, ctx->ev_dense[c], 0));
+      launch_dense(table, (int)D, Ic, Ac, (int64_t)G * n, lr, (uint32_t)ctx->cfg.vocab,
+                   ctx->num_sms, ctx->s_side);
+      ++nlaunch;
+    }
+    CK(cudaEventRecord(ctx->ev_s4, ctx->s_side));
+    CK(cudaStreamWaitEvent(s, ctx->ev_s4, 0));
+    LAUNCHED(nlaunch);
+    end_call(ctx);
+    return LMSCALE_OK;
   }
   launch_dense(table, (int)D, I, A, (int64_t)G * k, lr, (uint32_t)ctx->cfg.vocab, ctx->num_sms,
                s);
@@ -1297,6 +1327,9 @@ lmscale_status lmscale_get_stats(const lmscale_ctx* cctx, lmscale_stats* out) {
   if (ctx->timing_valid && ctx->tmode == 1) {
     CK(cudaEventSynchronize(ctx->tev[EV_SCATTER_END]));
     st.us_scatter = 1e3 * ev_ms(ctx, EV_S3_END, EV_SCATTER_END);
+  } else if (ctx->timing_valid && ctx->tmode == 3) {
+    CK(cudaEventSynchronize(ctx->tev[EV_AR_END]));
+    st.us_allreduce = 1e3 * ev_ms(ctx, EV_FIXUP_END, EV_AR_END);
   } else if (ctx->timing_valid && ctx->tmode == 2) {
     CK(cudaEventSynchronize(ctx->tev[EV_AR_END]));
     if (ctx->update_timed) CK(cudaEventSynchronize(ctx->tev[EV_UPD_END]));

@@ -257,3 +257,15 @@ def test_lookup_vs_numpy_and_special_cases():
     out = oracle.lookup(E, np.array([1, 97, 2**32 - 1], np.uint32))
     np.testing.assert_array_equal(out[0], E[1])
     assert (out[1:] == 0).all()
+
+
+def test_threaded_oracle_is_bit_identical():
+    """The all-cores timing variant (step 2 split over column blocks) computes
+    the same seven steps with the same per-element order: bit-identical."""
+    rng = np.random.default_rng(11)
+    J = [synth.zipf_ids(4000, 1.0, 2500, rank=g) for g in range(3)]
+    Dl = [rng.standard_normal((2500, 29)).astype(np.float32) for _ in range(3)]
+    a = oracle.sync_unique(J, Dl, np.zeros((4000, 29), np.float32), 0.1)
+    for t in (1, 4, 29, 64):
+        b = oracle.sync_unique_threads(J, Dl, np.zeros((4000, 29), np.float32), 0.1, t)
+        assert np.array_equal(a["Mhat64"], b["Mhat64"]) and np.array_equal(a["E"], b["E"])
