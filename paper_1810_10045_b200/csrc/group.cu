@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
   const int K = a.K, nb = gridDim.x;
   const uint32_t per = (uint32_t)((a.W + nb - 1) / nb);  // bitmap words per PC range
   gstamp(a.trace, 0);
+
   if (gtid == 0) {
     a.sc->err = 0u;
     a.sc->u_local = 0;
@@ -231,26 +232,18 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
   {
     const int64_t w0 = (int64_t)blockIdx.x * per;
     const int64_t w1 = min(a.W, w0 + (int64_t)per);
-    uint32_t pu = 0, pt = 0, ru = 0, rt = 0;
-    for (int c = tid; c < nb; c += GT) {
-      uint32_t cu = 0, ct = 0;
+    // this range's prefix: the totals of every earlier range (all stripes)
+    uint32_t pu = 0, pt = 0;
+    for (int c = tid; c < (int)blockIdx.x; c += GT) {
 #pragma unroll
       for (int sI = 0; sI < NST; ++sI) {
-        cu += __ldcg(a.ctot + (size_t)sI * 2 * nb + 2 * c);
-        ct += __ldcg(a.ctot + (size_t)sI * 2 * nb + 2 * c + 1);
+        pu += __ldcg(a.ctot + (size_t)sI * 2 * nb + 2 * c);
+        pt += __ldcg(a.ctot + (size_t)sI * 2 * nb + 2 * c + 1);
       }
-      if (c < (int)blockIdx.x) {
-        pu += cu;
-        pt += ct;
-      }
-      ru += cu;  // grand totals: U_i and the valid tokens
-      rt += ct;
     }
     uint32_t ea, eb, ta, tb;
     block_scan2(pu, pt, ea, eb, ta, tb, s_a, s_b);
     const uint32_t cta_u = ta, cta_t = tb;
-    block_scan2(ru, rt, ea, eb, ta, tb, s_a, s_b);
-    const uint32_t tot_u = ta, tot_t = tb;
     gstamp(a.trace, 7);
     const int nwarps = GT / 32;
     const int64_t nw = w1 > w0 ? w1 - w0 : 0;
@@ -329,12 +322,13 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
       }
       __syncwarp();
     }
-    if (blockIdx.x == 0 && tid == 0) {
-      a.sc->u_local = tot_u;
-      a.lstart[tot_u] = (int32_t)tot_t;
-      a.runfirst[a.nr] = (int32_t)tot_u;
-      if (a.nu_out) *a.nu_out = tot_u;
-      if (a.sc3) a.sc3->u_global = tot_u;
+    // the last range ends at U_i (ids) and the valid token count
+    if (blockIdx.x == nb - 1 && warp == nwarps - 1 && lane == 0) {
+      a.sc->u_local = bu;
+      a.lstart[bu] = (int32_t)bt;
+      a.runfirst[a.nr] = (int32_t)bu;
+      if (a.nu_out) *a.nu_out = bu;
+      if (a.sc3) a.sc3->u_global = bu;
     }
   }
   gstamp(a.trace, 3);

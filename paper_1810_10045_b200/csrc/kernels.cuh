@@ -92,7 +92,7 @@ struct G1Args {
   uint32_t* ihat;
   int32_t* l2g;
   Sc3* sc3;
-  GridBar* bar;
+  GridBar* bar;     // in-kernel grid barrier (zeroed at init)
 };
 cudaError_t launch_group(const G1Args& a, int num_sms, cudaStream_t s);
 

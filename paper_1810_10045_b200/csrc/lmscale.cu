@@ -97,7 +97,7 @@ struct lmscale_ctx {
   void* ck_dev = nullptr;      // FLAG_CHECK scratch: (U_g, checksum) x (1 + world)
   float cF = 0.f;              // compression scale (0: off), lmscale_set_compression
   int cbf = 0;                 // codec: 0 binary16, 1 bfloat16 (lmscale_set_codec)
-  GridBar* bars = nullptr;     // in-kernel grid barriers: [0] S4, [1] S1, [2] S3
+  GridBar* bars = nullptr;     // in-kernel grid barriers: [1] S1, [2] S3
   float* table_ptr = nullptr;  // lmscale_alloc_table
   size_t table_bytes = 0;
   bool table_nccl = false;

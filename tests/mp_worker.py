@@ -273,8 +273,11 @@ def compressed_row(Js, Ds, w, F):
     return oracle.decompress(oracle.compress(s, F), F)
 
 
-def run_full(cfg, rank, G, dev, n_rand=24, fused=False, F=0.0):
-    """BASELINE full size on G real GPUs: integers in full, sampled float rows."""
+def run_full(cfg, rank, G, dev, n_rand=24, fused=False, F=0.0, own_table=False):
+    """BASELINE full size on G real GPUs: integers in full, sampled float rows.
+    own_table: the table in the context's symmetric window (lmscale_alloc_table),
+    i.e. the launch configuration bench.py times (P2P fused S5+S6, local-slot M,
+    S4 beside the peer-bitmap S3)."""
     mode = "signed"
     lr = synth.default_lr(mode)
     if F > 0:
@@ -282,13 +285,21 @@ def run_full(cfg, rank, G, dev, n_rand=24, fused=False, F=0.0):
     J = [synth.ids_for(cfg, g) for g in range(G)]
     ctx = make_context(cfg.V, cfg.K, cfg.D)
     grad = synth.grad_values(cfg.K, cfg.D, mode, rank=rank, device=dev)
-    E = synth.table_values(cfg.V, cfg.D, mode, device=dev)
+    if own_table:
+        E = ctx.alloc_table()
+        E.copy_(synth.table_values(cfg.V, cfg.D, mode, device=dev))
+        torch.cuda.synchronize()
+    else:
+        E = synth.table_values(cfg.V, cfg.D, mode, device=dev)
     Ihat, gcounts = oracle.unique_global(np.concatenate(J))
     if F > 0:
         ctx.set_compression(F)
     if fused:
         ctx.step(torch.from_numpy(J[rank].view(np.int32)).to(dev), grad, E, lr)
         torch.cuda.synchronize()
+        st = ctx.stats()
+        if own_table:   # the P2P kernels (compressed or not), as bench.py runs them
+            assert st["fused_s5_s6"] == (3 if F > 0 else 2), st["fused_s5_s6"]
         ids = u32(ctx.sparse_grad().ids)
         rows = None
     else:
@@ -324,6 +335,32 @@ def run_full(cfg, rank, G, dev, n_rand=24, fused=False, F=0.0):
         check_rows(gotE[i:i + 1], (E0[i] - lr * ref)[None], (np.abs(E0[i]) + lr * A)[None],
                    "signed", f"{cfg.name} G={G} E row {w}")
     check_replicas(E, f"full {cfg.name}")
+    if rank == 0:
+        print(f"full {cfg.name} G={G} fused={fused} F={F} own_table={own_table} "
+              f"words={len(words)}", flush=True)
+    ctx.close()
+
+
+def run_compressed_discriminating(rank, G, dev):
+    """R15 on real GPUs: one word, rank 0 contributes 2049, rank 1 contributes
+    1, the others 0 (F = 1): the codec on each transfer gives 2049 -> 2048
+    (sender), 2049 -> 2048 (owner's sum), so every replica holds -2048; a codec
+    applied once to the exact sum would give -2050."""
+    D = 8
+    ctx = make_context(16, 4, D)
+    ctx.set_compression(1.0)
+    E = ctx.alloc_table()
+    E.zero_()
+    val = {0: 2049.0, 1: 1.0}.get(rank, 0.0)
+    g = torch.full((1, D), val, dtype=torch.float32, device=dev)
+    ids = torch.tensor([3], dtype=torch.int32, device=dev)
+    ctx.step(ids, g, E, 1.0)
+    torch.cuda.synchronize()
+    assert torch.all(E[3] == -2048.0), E[3]
+    assert torch.count_nonzero(E) == D
+    check_replicas(E, "compressed 2049+1")
+    if rank == 0:
+        print(f"compressed 2049+1 -> 2048 G={G}", flush=True)
     ctx.close()
 
 
@@ -364,6 +401,14 @@ def main():
         run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "int", rank, G, dev, 1.0, fmt="bf16")
         run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "signed", rank, G, dev, 1.0,
                              own_table=True, fmt="bf16")
+    if "p2p" in which:
+        # the launch configuration bench.py times (table window, P2P fused
+        # S5+S6), fp32 and compressed, at 1b and tieba full size
+        run_compressed_discriminating(rank, G, dev)
+        for name in ("1b", "tieba"):
+            run_full(synth.CONFIGS[name], rank, G, dev, n_rand=400, fused=True, own_table=True)
+            run_full(synth.CONFIGS[name], rank, G, dev, n_rand=200, fused=True, own_table=True,
+                     F=1.0)
     for name in ("1b", "char", "amazon", "tieba"):
         if name in which:
             run_full(synth.CONFIGS[name], rank, G, dev)

@@ -130,6 +130,28 @@ def test_exchange_rounds_when_not_exact():
     assert got["Mhat"][0, 0] == 8416.0
 
 
+def test_exchange_codec_on_each_transfer_discriminates():
+    """R15's reading -- the codec on each of the two transfers (sender payload,
+    then the owner's reduced row) -- against a codec applied once to the exact
+    sum: G = 2, one word, rank 0 contributes 2049, rank 1 contributes 1, F = 1.
+    Two-stage: 2049 -> 2048 (binary16 RNE, tie to even), 1 -> 1, fp32 sum
+    2049 -> 2048.  Single-stage would give compress(2050) = 2050.  A dropped
+    sender-side codec would also give 2050; a ring that re-rounds partial
+    sums hop by hop is not what the exchange does (R15)."""
+    J = [np.array([3], np.uint32), np.array([3], np.uint32)]
+    Dl = [np.array([[2049.0]], np.float32), np.array([[1.0]], np.float32)]
+    E0 = np.zeros((5, 1), np.float32)
+    got = oracle.sync_unique_compressed(J, Dl, E0.copy(), 1.0, 1.0)
+    assert got["Q"][0][0, 0] == np.float16(2048.0).view(np.uint16)     # sender rounding
+    assert got["S"][0, 0] == 2049.0                                     # fp32 owner sum
+    assert got["Mhat"][0, 0] == 2048.0                                  # second rounding
+    assert got["E"][3, 0] == -2048.0
+    plain = oracle.sync_unique(J, Dl, E0.copy(), 1.0)
+    assert plain["Mhat64"][0, 0] == 2050.0
+    single = oracle.decompress(oracle.compress(np.float32([2050.0]), 1.0), 1.0)
+    assert single[0] == 2050.0 != got["Mhat"][0, 0]
+
+
 @pytest.mark.parametrize("G", [2, 4])
 @pytest.mark.parametrize("F", [1.0, 32.0])
 def test_exchange_error_bound_signed(G, F):
