@@ -90,6 +90,7 @@ struct NvlsKernelArgs {
   size_t mhat_off;    // byte offset of the compressed M^ rows in the M window
   size_t lrank_off;   // local-slot layout: byte offset of lrank in the window
   int local_m;        // 1: M_j rows are at rank j's local index (lrank + popcount), else at r
+  int pb_slots;       // k_p2p_bulk: shared-memory ring slots
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -283,6 +284,137 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
 }
 
 
+// S5+S6 over NVLink with the row traffic on the TMA engine (default P2P
+// kernel for dim % 4 == 0): each CTA owns a contiguous block of this rank's
+// rows r = rank + G t.  After the first LSA barrier, the CTA looks up, for all
+// its rows at once, which ranks hold word I^[r] (peers' presence bitmaps) and
+// where (lrank + popcount); then a producer warp streams, per (row, column
+// block of <= 2 KB), the present copies of M[r] from the peers' windows and
+// the local E block into a shared-memory slot with cp.async.bulk (one
+// mbarrier per slot), while consumer threads sum the copies in rank order,
+// form fma(-lr, m, e) and store it into every replica of the table.  Bytes in
+// flight cost no registers, and no per-row chain of remote loads remains.
+constexpr int PB_CB = 512;        // floats per column block (2 KB)
+constexpr int PB_MAXROWS = 1024;  // owned rows per CTA (presence table in smem)
+constexpr int PB_THREADS = PB_CB / 4 + 32;
+constexpr int PB_MAXSLOTS = 16;
+constexpr int PB_MAX_CPS = 4;     // k_p2p_bulk CTAs per SM (LSA barrier count)
+
+__global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
+  constexpr int MAXG = 8;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[2 * PB_MAXSLOTS];
+  __shared__ uint32_t s_w[PB_MAXROWS];
+  __shared__ uint8_t s_has[PB_MAXROWS];
+  const int G = a.world, tid = threadIdx.x, nct = PB_CB / 4;
+  const int NS = a.pb_slots;
+  const uint32_t SB = (uint32_t)(G + 1) * PB_CB * 4;  // a slot: <= G copies + the E block
+  uint32_t* s_lrow = reinterpret_cast<uint32_t*>(smem + (size_t)NS * SB);  // [rows][G]
+  (void)0;
+  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8u * PB_MAXSLOTS;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full0 + 8u * s, 1u);
+      mbar_init(empty0 + 8u * s, (uint32_t)(nct / 32));
+    }
+    fence_mbar_init();
+  }
+  ncclCoopCta cta;
+  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
+                                         /*multimem=*/true);
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  if (__ldcg(&a.sc3->err) & 1u) return;      // id error on some rank: all ranks leave
+  const int64_t Ug = a.sc3->u_global;
+  const int64_t T = Ug > a.rank ? (Ug - a.rank + G - 1) / G : 0;  // this rank's rows
+  const int64_t t0 = T * blockIdx.x / gridDim.x, t1 = T * (blockIdx.x + 1) / gridDim.x;
+  const int D = a.D;
+  const int ncb = (D + PB_CB - 1) / PB_CB;
+  const int lane = tid & 31;
+  int it0 = 0;  // items issued / consumed before this batch (ring phase continuity)
+  for (int64_t b0 = t0; b0 < t1; b0 += PB_MAXROWS) {
+    const int nrows = (int)(t1 - b0 < PB_MAXROWS ? t1 - b0 : PB_MAXROWS);
+    // ---- presence and row of word I^[r] on every rank, for the batch's rows
+    for (int i = tid; i < nrows; i += blockDim.x) {
+      const int64_t r = a.rank + (int64_t)G * (b0 + i);
+      const uint32_t w = __ldg(a.ihat + r);
+      uint32_t has = 0;
+      for (int j = 0; j < G; ++j) {
+        const char* base = reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j));
+        const uint32_t bits =
+            __ldcv(reinterpret_cast<const uint32_t*>(base + a.lbits_off) + (w >> 5));
+        has |= ((bits >> (w & 31u)) & 1u) << j;
+        uint32_t lrow = (uint32_t)r;
+        if (a.local_m)
+          lrow = __ldcv(reinterpret_cast<const uint32_t*>(base + a.lrank_off) + (w >> 5)) +
+                 __popc(bits & ((1u << (w & 31u)) - 1u));
+        s_lrow[i * G + j] = lrow;
+      }
+      s_w[i] = w;
+      s_has[i] = (uint8_t)has;
+    }
+    __syncthreads();
+    const int items = nrows * ncb;
+    if (tid >= nct) {
+      // -------------------------------------------------------- producer warp
+      const char* pm =
+          (lane < G) ? reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, lane)) : nullptr;
+      for (int q = 0; q < items; ++q) {
+        const int it = it0 + q;
+        const int s = it % NS, ph = it / NS;
+        if (ph > 0) mbar_wait(empty0 + 8u * s, (uint32_t)(ph - 1) & 1u);
+        const int i = q / ncb, cb = q % ncb;
+        const int cw = min(PB_CB, D - cb * PB_CB);
+        const uint32_t bytes = (uint32_t)cw * 4u;
+        const uint32_t has = s_has[i];
+        const int n = __popc(has);
+        if (lane == 0) mbar_arrive_tx(full0 + 8u * s, (uint32_t)(n + 1) * bytes);
+        __syncwarp();
+        const uint32_t dst = smem_u32(smem) + (uint32_t)s * SB;
+        if (lane < G && ((has >> lane) & 1u)) {
+          const int k = __popc(has & ((1u << lane) - 1u));  // rank order
+          bulk_g2s(dst + (uint32_t)k * PB_CB * 4,
+                   pm + ((size_t)s_lrow[i * G + lane] * D + (size_t)cb * PB_CB) * 4, bytes,
+                   full0 + 8u * s);
+        }
+        if (lane == 31)
+          bulk_g2s(dst + (uint32_t)n * PB_CB * 4,
+                   a.table + (size_t)s_w[i] * D + (size_t)cb * PB_CB, bytes, full0 + 8u * s);
+      }
+    } else {
+      // ----------------------------------------------------------- consumers
+      float4* pe[MAXG];
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j)
+        pe[j] = j < G ? reinterpret_cast<float4*>(ncclGetLsaPointer(a.twin, 0, j)) : nullptr;
+      const int t = tid;
+      for (int q = 0; q < items; ++q) {
+        const int it = it0 + q;
+        const int s = it % NS, ph = it / NS;
+        const int i = q / ncb, cb = q % ncb;
+        const int cw = min(PB_CB, D - cb * PB_CB) / 4;
+        mbar_wait(full0 + 8u * s, (uint32_t)ph & 1u);
+        if (t < cw) {
+          const float4* slot = reinterpret_cast<const float4*>(smem + (size_t)s * SB);
+          const int n = __popc((uint32_t)s_has[i]);
+          float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 0; k < n; ++k) m = add4(m, slot[k * (PB_CB / 4) + t]);  // rank order
+          const float4 e = fma4(-a.lr, m, slot[n * (PB_CB / 4) + t]);
+          const size_t off = ((size_t)s_w[i] * D + (size_t)cb * PB_CB) / 4 + t;
+#pragma unroll
+          for (int j = 0; j < MAXG; ++j)
+            if (j < G) __stcg(pe[j] + off, e);
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(empty0 + 8u * s);
+      }
+    }
+    it0 += items;
+    __syncthreads();  // the batch's presence table is no longer read
+  }
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
+}
+
+
 // Compressed S5+S6 (Sec. 3.3; R15): the all-reduce as a
 // reduce-scatter and an all-gather, each carrying binary16 payloads.
 //   1. LSA barrier: every rank's compressed M_g (written by S4) is complete;
@@ -427,7 +559,7 @@ NvlsState* nvls_create(ncclComm_t comm, void* M, size_t bytes, int num_sms, char
   }
   ncclDevCommRequirements req{};
   req.lsaMultimem = true;
-  req.lsaBarrierCount = st->ctas;
+  req.lsaBarrierCount = PB_MAX_CPS * st->ctas;  // k_p2p_bulk runs up to PB_MAX_CPS CTAs per SM
   r = ncclDevCommCreate(comm, &req, &st->dev);
   if (r != ncclSuccess) {
     snprintf(err, errlen, "ncclDevCommCreate(lsaMultimem): %s", ncclGetErrorString(r));
@@ -530,10 +662,33 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
     else
       k_p2p_update_c<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
   } else if (twin && nvls_use_p2p(world)) {
-    if (v4)
+    static const bool no_bulk = getenv("LMSCALE_NO_P2P_BULK") != nullptr;
+    const bool bulk = v4 && !no_bulk && (uintptr_t)M % 16 == 0;
+    if (bulk) {
+      // ring: (G + 1) x 2 KB per slot; the rest of the CTA's share of shared
+      // memory after the presence table
+      const size_t sb = (size_t)(world + 1) * PB_CB * 4;
+      const size_t lrow_bytes = 4 * (size_t)PB_MAXROWS * world;
+      static const int cps_env =
+          getenv("LMSCALE_P2P_CTAS_PER_SM") ? atoi(getenv("LMSCALE_P2P_CTAS_PER_SM")) : 0;
+      const int cps = cps_env >= 1 && cps_env <= PB_MAX_CPS ? cps_env : 4;  // measured best (tools/ab_p2p.sh)
+      int slots = (int)(((size_t)200 * 1024 / cps - lrow_bytes) / sb);
+      slots = slots < 2 ? 2 : slots > PB_MAXSLOTS ? PB_MAXSLOTS : slots;
+      a.pb_slots = slots;
+      const size_t smem = (size_t)slots * sb + lrow_bytes;
+      static size_t set = 0;
+      if (smem > set) {
+        cudaFuncSetAttribute(k_p2p_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        set = smem;
+      }
+      // two CTAs per SM: one CTA's bulk-copy stream saturates well below
+      // the SM's share (tools/gather_probe.cu)
+      k_p2p_bulk<<<cps * st->ctas, PB_THREADS, smem, s>>>(a);
+    } else if (v4) {
       k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
-    else
+    } else {
       k_p2p_update<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
+    }
   } else if (v4) {
     k_nvls_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
   } else {
