@@ -681,8 +681,8 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
         cudaFuncSetAttribute(k_p2p_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         set = smem;
       }
-      // two CTAs per SM: one CTA's bulk-copy stream saturates well below
-      // the SM's share (tools/gather_probe.cu)
+      // several CTAs per SM (one CTA's bulk-copy stream saturates below the
+      // SM's share: tools/gather_probe.cu)
       k_p2p_bulk<<<cps * st->ctas, PB_THREADS, smem, s>>>(a);
     } else if (v4) {
       k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
