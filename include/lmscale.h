@@ -354,7 +354,7 @@ LMSCALE_API lmscale_status lmscale_get_stats(const lmscale_ctx* ctx, lmscale_sta
 LMSCALE_API const char* lmscale_status_string(lmscale_status s);
 /* Last detailed error message of this context (static storage inside ctx). */
 LMSCALE_API const char* lmscale_last_error(const lmscale_ctx* ctx);
-/* Library version string, e.g. "lmscale 0.1 sm_100a". */
+/* Library version string, e.g. "lmscale 0.2 sm_100a" ("+device-checks" for the checked build). */
 LMSCALE_API const char* lmscale_version(void);
 
 #ifdef __cplusplus

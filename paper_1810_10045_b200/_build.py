@@ -16,6 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblmscale.so")
+LIB_CHECKED = os.path.join(PKG, "liblmscale_checked.so")  # device bounds checks compiled in
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -34,20 +35,24 @@ def _deps():
         os.path.join(ROOT, "include", "lmscale.h"), __file__]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(path: str = LIB) -> bool:
+    if not os.path.exists(path):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(path)
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked: the LMSCALE_DEVICE_CHECKS build (bounds asserts in the kernels)
+    as liblmscale_checked.so; load it with LMSCALE_LIB=<path>."""
+    out = LIB_CHECKED if checked else LIB
+    if not force and up_to_date(out):
+        return out
     inc, lib = nccl_dirs()
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [nvcc, "-O3", "-std=c++17", "-lineinfo", *ARCH, "-shared", "-Xcompiler", "-fPIC",
+           *(["-DLMSCALE_DEVICE_CHECKS"] if checked else []),
            "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            *sources(), "-L", lib, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}",
@@ -56,9 +61,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                checked="--checked" in sys.argv))

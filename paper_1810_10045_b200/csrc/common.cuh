@@ -5,7 +5,26 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
+
+// Device-side bounds checks of the checked build (LMSCALE_DEVICE_CHECKS,
+// `python -m paper_1810_10045_b200._build --checked` -> liblmscale_checked.so):
+// the stand-in for compute-sanitizer, which is closed on this GPU pool.  A
+// failed check prints the condition and traps (the launch fails with an
+// error); in the product build the checks compile to nothing.
+#ifdef LMSCALE_DEVICE_CHECKS
+#define LMS_CHECK(cond)                                                              \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("LMS_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                            \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define LMS_CHECK(cond) ((void)0)
+#endif
 
 namespace lms {
 

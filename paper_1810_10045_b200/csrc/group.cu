@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
 #pragma unroll
       for (int q = 0; q < SPT; ++q) {
         if (key[q] == EMPTY) continue;
+        LMS_CHECK(key[q] < a.vocab && base[q] + cnt[q] <= (uint32_t)a.K);
         h_cnt[tid + q * GT] = base[q];
         const int r = (int)((key[q] >> 5) / per);  // 32-bit division
         if (base[q] == 0u) {
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
         if (has) {
           const uint32_t id = (uint32_t)(w * 32 + lane);
           const uint32_t u = bu + __popc(bits & lanemask_lt());
+          LMS_CHECK(u < (uint32_t)a.K && bt + inc <= (uint32_t)a.K && id < a.vocab);
           a.luniq[u] = id;
           a.counts[u] = (int32_t)cnt;
           a.lstart[u] = (int32_t)(bt + inc - cnt);
@@ -375,6 +377,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
       const int i = tid + k * GT;
       if (i < n && id[k] < a.vocab) {
         const uint32_t spos = (uint32_t)__ldcg(a.lstart + base[k]) + t[k];
+        LMS_CHECK(spos < (uint32_t)a.K && spos / a.seg_len <= (uint32_t)a.nr);
         a.perm[spos] = sub + i;
         // the S4 range starting here begins inside run u
         if (spos % a.seg_len == 0u) a.runfirst[spos / a.seg_len] = (int32_t)base[k];

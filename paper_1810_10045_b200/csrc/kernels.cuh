@@ -132,6 +132,8 @@ struct SegArgs {
   unsigned long long* trace;  // LMSCALE_PHASE_TRACE stamps (or nullptr)
   int K, D, num_sms;
   uint32_t seg_len;       // set by launch_seg: grouped positions per range
+  uint32_t vocab;         // bounds of the checked build (LMS_CHECK)
+  int64_t mrows, part_rows;
   int cbw, nct, gr, nslot, neslot, lmax;
 };
 struct SegPlan {
@@ -184,7 +186,7 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
                         float cF, int cbf, size_t mhat_off, size_t lrank_off, int local_m,
-                        cudaStream_t s);
+                        int64_t mcap, uint32_t vocab, cudaStream_t s);
 // true: the peer-to-peer fused kernel (presence-aware) is used for this G
 bool nvls_use_p2p(int world);
 // LSA base of every rank's M window (world entries written to out_host)

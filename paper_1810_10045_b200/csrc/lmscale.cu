@@ -352,6 +352,9 @@ lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
   a.D = (int)ctx->cfg.dim;
   a.num_sms = ctx->num_sms;
   a.trace = ctx->trace;
+  a.vocab = (uint32_t)ctx->cfg.vocab;
+  a.mrows = ctx->ucap;
+  a.part_rows = 2 * ctx->nr_max;
   CK(launch_seg(a, s));
   LAUNCHED(1);
   if (world1) ctx->lbits_clean = true;
@@ -383,7 +386,13 @@ float ev_ms(const lmscale_ctx* c, int a, int b) {
 
 extern "C" {
 
-const char* lmscale_version(void) { return "lmscale 0.1 sm_100a"; }
+const char* lmscale_version(void) {
+#ifdef LMSCALE_DEVICE_CHECKS
+  return "lmscale 0.2 sm_100a +device-checks";
+#else
+  return "lmscale 0.2 sm_100a";
+#endif
+}
 
 const char* lmscale_status_string(lmscale_status s) {
   switch (s) {
@@ -985,7 +994,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
                        ctx->cfg.rank, G, ctx->trace,
                        table == ctx->table_ptr ? ctx->table_win : nullptr, ctx->lbits_off,
                        comp ? ctx->cF : 0.f, ctx->cbf, ctx->mhat_off, ctx->lrank_off,
-                       local_m ? 1 : 0, s);
+                       local_m ? 1 : 0, ctx->ucap, (uint32_t)ctx->cfg.vocab, s);
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {

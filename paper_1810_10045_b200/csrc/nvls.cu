@@ -91,6 +91,8 @@ struct NvlsKernelArgs {
   size_t lrank_off;   // local-slot layout: byte offset of lrank in the window
   int local_m;        // 1: M_j rows are at rank j's local index (lrank + popcount), else at r
   int pb_slots;       // k_p2p_bulk: shared-memory ring slots
+  int64_t mcap;       // rows of every rank's M (bounds of the checked build)
+  uint32_t vocab;
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -347,8 +349,10 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
         if (a.local_m)
           lrow = __ldcv(reinterpret_cast<const uint32_t*>(base + a.lrank_off) + (w >> 5)) +
                  __popc(bits & ((1u << (w & 31u)) - 1u));
+        LMS_CHECK(lrow < (uint32_t)a.mcap);
         s_lrow[i * G + j] = lrow;
       }
+      LMS_CHECK(w < a.vocab);
       s_w[i] = w;
       s_has[i] = (uint8_t)has;
     }
@@ -626,8 +630,10 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
                         float cF, int cbf, size_t mhat_off, size_t lrank_off, int local_m,
-                        cudaStream_t s) {
+                        int64_t mcap, uint32_t vocab, cudaStream_t s) {
   NvlsKernelArgs a;
+  a.mcap = mcap;
+  a.vocab = vocab;
   a.cbf = cbf;
   a.lrank_off = lrank_off;
   a.local_m = local_m;

@@ -132,6 +132,7 @@ __device__ __forceinline__ void cut_piece(const SegArgs& a, Meta& m, bool head, 
   const int np = b1 - b0 + 1;
   const int k = b - b0;  // this piece
   const size_t prow = k == 0 ? (size_t)(2 * b0 + 1) : (size_t)(2 * b);
+  LMS_CHECK(k >= 0 && np >= 1 && prow < (size_t)a.part_rows && b1 < (int)gridDim.x);
   if (act) __stcg(reinterpret_cast<T*>(a.part + prow * D + col), acc);
   const int j = k / SEG_FXP, ng = (np + SEG_FXP - 1) / SEG_FXP;
   const int gn = min(SEG_FXP, np - j * SEG_FXP);
@@ -237,7 +238,10 @@ __global__ void __launch_bounds__(SEG_MAX_THREADS) k_seg(SegArgs a) {
   const int L = p1 - p0;
   // ---- prologue: the range's rows, its runs (from S1's run starts), the
   // segment ends and what each end emits to
-  for (int i = tid; i < L; i += blockDim.x) s_pos[i] = (uint32_t)__ldg(a.perm + p0 + i);
+  for (int i = tid; i < L; i += blockDim.x) {
+    s_pos[i] = (uint32_t)__ldg(a.perm + p0 + i);
+    LMS_CHECK(s_pos[i] < (uint32_t)K);
+  }
   const int u0 = __ldg(a.runfirst + b);
   const int un = __ldg(a.runfirst + b + 1);  // run holding p1 (or U at the end)
   const int ul = __ldg(a.lstart + un) == p1 ? un - 1 : un;  // run holding p1 - 1
@@ -246,6 +250,7 @@ __global__ void __launch_bounds__(SEG_MAX_THREADS) k_seg(SegArgs a) {
     const int u = u0 + r;
     const int st = __ldg(a.lstart + u), en = __ldg(a.lstart + u + 1);
     const int e = min(en, p1) - 1 - p0;  // this range's last position of run u
+    LMS_CHECK(e >= 0 && e < L && st < en && st <= p1 - 1);
     uint32_t f = F_END;
     if (st >= p0 && en <= p1) {
       f |= F_FULL;
@@ -323,6 +328,7 @@ __global__ void __launch_bounds__(SEG_MAX_THREADS) k_seg(SegArgs a) {
       if (f & F_END) {
         if (f & F_FULL) {
           const uint32_t wv = s_w[i0 + j];
+          LMS_CHECK(a.apply ? wv < a.vocab : (int)wv < 0 || (int64_t)wv < a.mrows);
           if (a.apply) {
             T* dst = reinterpret_cast<T*>(a.table + (size_t)wv * D + col);
             if (act)

@@ -13,7 +13,9 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblmscale.so")
+# LMSCALE_LIB selects another in-tree build (e.g. liblmscale_checked.so, the
+# device-bounds-checked build); there is no fallback to anything else
+LIB_PATH = os.environ.get("LMSCALE_LIB") or os.path.join(_PKG, "liblmscale.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
