@@ -22,7 +22,8 @@
 //   PD  per token p: u = lrank[w] + popc(bits below) (the inverse map),
 //       grouped position lstart[u] + ticket[p]: perm, the grouped order that
 //       S4 walks; the token at the first position of an S4 range records the
-//       range's first run (runfirst); wcount returns to zero.
+//       range's first run (runfirst).  (wcount returns to zero in PC, once per
+//       present id.)
 //
 // Two grid barriers in a normally-launched kernel sized to co-residency (one
 // CTA per SM).  The grouping is a counting sort, so the tokens of one word are
@@ -103,7 +104,10 @@ __device__ __forceinline__ uint32_t hslot(uint32_t id) { return (id * 0x9E3779B1
 
 // wcount is stored transposed (index (id % 32) * W + id / 32): consecutive ids
 // -- the Zipf head of a frequency-ordered vocabulary -- fall in different
-// cache lines, so the chunks' atomics on hot ids do not queue on one line.
+// cache lines, so the chunks' atomics on hot ids do not queue on one line,
+// and PC's loads of a 32-word chunk (lane = word, fixed bit) stay coalesced.
+// (A multiplicative-hash layout spread the atomics further -- tieba PA 6.3 ->
+// 5.1 us -- but made every PC load scattered: amazon PC 10 -> 37 us.)
 __device__ __forceinline__ size_t widx(uint32_t id, int64_t W) {
   return (size_t)(id & 31u) * (size_t)W + (id >> 5);
 }
@@ -190,10 +194,13 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
       for (int q = 0; q < SPT; ++q)
         base[q] = key[q] != EMPTY ? atomicAdd(a.wcount + widx(key[q], a.W), cnt[q]) : 0u;
 #pragma unroll
+      for (int q = 0; q < SPT; ++q)
+        if (key[q] != EMPTY) h_cnt[tid + q * GT] = base[q];
+      gstamp(a.trace, 13);
+#pragma unroll
       for (int q = 0; q < SPT; ++q) {
         if (key[q] == EMPTY) continue;
         LMS_CHECK(key[q] < a.vocab && base[q] + cnt[q] <= (uint32_t)a.K);
-        h_cnt[tid + q * GT] = base[q];
         const int r = (int)((key[q] >> 5) / per);  // 32-bit division
         if (base[q] == 0u) {
           atomicOr(a.lbits + (key[q] >> 5), 1u << (key[q] & 31u));
@@ -255,13 +262,21 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     // each load is coalesced) into a padded 32 x 33 tile, then read back
     // lane = bit for the scans and the coalesced emission.
     uint32_t* tile = g_smem + warp * (32 * 33);
-    auto load_chunk = [&](int64_t xc, uint32_t& mybits) -> uint32_t {
+    // (the counts are returned to zero right after they are read, once per
+    // id -- zeroing them per token in PD queued thousands of stores on the
+    // Zipf head's counters: 15 us at tieba)
+    auto load_chunk = [&](int64_t xc, uint32_t& mybits, bool zero) -> uint32_t {
       const int64_t myw = xc + lane;
       mybits = myw < x1 ? __ldcg(a.lbits + myw) : 0u;
       uint32_t v[32], tot = 0;
 #pragma unroll
       for (int i = 0; i < 32; ++i)
         v[i] = ((mybits >> i) & 1u) ? __ldcg(a.wcount + (size_t)i * a.W + myw) : 0u;
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if ((mybits >> i) & 1u) a.wcount[(size_t)i * a.W + myw] = 0u;
+      }
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         tile[i * 33 + lane] = v[i];
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     const bool one_chunk = x1 - x0 <= 32;
     for (int64_t xc = x0; xc < x1; xc += 32) {
       uint32_t mybits;
-      wt += load_chunk(xc, mybits);
+      wt += load_chunk(xc, mybits, one_chunk);
       wu += __popc(mybits);
       bits0 = mybits;
       __syncwarp();
@@ -293,7 +308,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     // pass 2: emit J^, counts, lstart, lrank (lane = bit: coalesced stores)
     for (int64_t xc = x0; xc < x1; xc += 32) {
       uint32_t mybits = bits0;
-      if (!one_chunk) load_chunk(xc, mybits);
+      if (!one_chunk) load_chunk(xc, mybits, true);
       const int nwc = (int)(x1 - xc < 32 ? x1 - xc : 32);
       for (int j = 0; j < nwc; ++j) {
         const int64_t w = xc + j;
@@ -381,7 +396,6 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
         a.perm[spos] = sub + i;
         // the S4 range starting here begins inside run u
         if (spos % a.seg_len == 0u) a.runfirst[spos / a.seg_len] = (int32_t)base[k];
-        a.wcount[widx(id[k], a.W)] = 0u;  // the count array returns to zero
       }
     }
   }

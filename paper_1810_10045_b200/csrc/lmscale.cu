@@ -573,6 +573,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     ctx->NI = (int64_t)cfg->world * cfg->max_tokens;
     ctx->ucap = std::min<int64_t>(ctx->NI, cfg->vocab);
     ctx->nr_max = seg_max_ranges(ctx->K, ctx->num_sms);
+
     const int64_t K = ctx->K, D = cfg->dim;
     // ---- workspace layout (one allocation, 256-byte aligned sub-buffers)
     size_t off = 0;
