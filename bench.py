@@ -355,7 +355,7 @@ class Bench:
         from paper_1810_10045_b200.distributed import max_over_ranks
         return max_over_ranks(x, self.dev)
 
-    def timed(self, fn, steps, warmup, collect=None):
+    def timed(self, fn, steps, warmup, collect=None, on_start=None):
         import torch
         for _ in range(warmup):
             self.flush_l2()
@@ -367,6 +367,8 @@ class Bench:
         if self.world > 1:          # one untimed step absorbs the ranks' start skew
             self.flush_l2()
             fn()
+        if on_start:
+            on_start()
         # steps are enqueued back to back (no host round trip between them);
         # each is bracketed by its own events, the L2 flush between steps is
         # outside them, and the step's own exchange keeps ranks in lock-step
@@ -460,9 +462,12 @@ class Bench:
         if clk:
             clk.start()
         load_window(0.3 if headline else 0.05)
-        k_before = ctx.stats()["kernels_total_lo"]
-        ms = self.timed(step, args.steps, 0)
-        launches = ctx.stats()["kernels_total_lo"] - k_before
+        k_before = [0]
+
+        def mark():
+            k_before[0] = ctx.stats()["kernels_total_lo"]
+        ms = self.timed(step, args.steps, 0, on_start=mark)
+        launches = ctx.stats()["kernels_total_lo"] - k_before[0]   # the timed steps' kernels
         if headline:
             load_window(0.1)
         clocks = clk.stop() if clk else None
