@@ -1003,8 +1003,8 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
       unsigned long long t[64];
       cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
       fprintf(stderr,
-              "[lmscale trace rank %d] nvls: barrier1 %.2f  reduce+update+bcast %.2f  barrier2 %.2f"
-              "  copy %.2f us | S3 start -> nvls start %.2f us\n",
+              "[lmscale trace rank %d] S5+S6: barrier1 %.2f  exchange+update %.2f  barrier2 %.2f"
+              "  tail %.2f us | S3 start -> S5+S6 start %.2f us\n",
               ctx->cfg.rank, (t[49] - t[48]) * 1e-3, (t[50] - t[49]) * 1e-3,
               (t[51] - t[50]) * 1e-3, (t[52] - t[51]) * 1e-3, (t[48] - t[32]) * 1e-3);
     }

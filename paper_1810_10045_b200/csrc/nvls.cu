@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
 
 
 // S5+S6 over NVLink with the row traffic on the TMA engine (default P2P
-// kernel for dim % 4 == 0): each CTA owns a contiguous block of this rank's
+// kernel for dim % 4 == 0): each CTA owns every gridDim-th of this rank's
 // rows r = rank + G t.  After the first LSA barrier, the CTA looks up, for all
 // its rows at once, which ranks hold word I^[r] (peers' presence bitmaps) and
 // where (lrank + popcount); then a producer warp streams, per (row, column
@@ -321,23 +321,29 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
     }
     fence_mbar_init();
   }
+  nv_stamp(a.trace, 48);
   ncclCoopCta cta;
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
                                          /*multimem=*/true);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  nv_stamp(a.trace, 49);
   if (__ldcg(&a.sc3->err) & 1u) return;      // id error on some rank: all ranks leave
   const int64_t Ug = a.sc3->u_global;
   const int64_t T = Ug > a.rank ? (Ug - a.rank + G - 1) / G : 0;  // this rank's rows
-  const int64_t t0 = T * blockIdx.x / gridDim.x, t1 = T * (blockIdx.x + 1) / gridDim.x;
+  // this CTA's rows: t = blockIdx.x + i * gridDim.x (interleaved: the Zipf head
+  // -- rows held by every rank, the most copies to load -- is spread over all
+  // CTAs; contiguous blocks left the first CTAs 40 % behind at tieba G = 2)
+  const int64_t nb = gridDim.x;
+  const int64_t nmine = T > (int64_t)blockIdx.x ? (T - blockIdx.x + nb - 1) / nb : 0;
   const int D = a.D;
   const int ncb = (D + PB_CB - 1) / PB_CB;
   const int lane = tid & 31;
   int it0 = 0;  // items issued / consumed before this batch (ring phase continuity)
-  for (int64_t b0 = t0; b0 < t1; b0 += PB_MAXROWS) {
-    const int nrows = (int)(t1 - b0 < PB_MAXROWS ? t1 - b0 : PB_MAXROWS);
+  for (int64_t b0 = 0; b0 < nmine; b0 += PB_MAXROWS) {
+    const int nrows = (int)(nmine - b0 < PB_MAXROWS ? nmine - b0 : PB_MAXROWS);
     // ---- presence and row of word I^[r] on every rank, for the batch's rows
     for (int i = tid; i < nrows; i += blockDim.x) {
-      const int64_t r = a.rank + (int64_t)G * (b0 + i);
+      const int64_t r = a.rank + (int64_t)G * ((int64_t)blockIdx.x + (b0 + i) * nb);
       const uint32_t w = __ldg(a.ihat + r);
       uint32_t has = 0;
       for (int j = 0; j < G; ++j) {
@@ -415,7 +421,10 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
     it0 += items;
     __syncthreads();  // the batch's presence table is no longer read
   }
+  nv_stamp(a.trace, 50);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
+  nv_stamp(a.trace, 51);
+  nv_stamp(a.trace, 52);
 }
 
 

@@ -30,8 +30,10 @@ if world > 1:
     dev = torch.device("cuda", local)
     ids = torch.from_numpy(synth.ids_for(cfg, rank).view(np.int32)).to(dev)
     grad = synth.grad_values(cfg.K, cfg.D, "signed", rank=rank, device=dev)
-    table = synth.table_values(cfg.V, cfg.D, "signed", device=dev)
-    ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_TIMING)
+    ctx = make_context(cfg.V, cfg.K, cfg.D,
+                       flags=0 if os.environ.get("TRACE_NO_EVENTS") else lmscale.FLAG_TIMING)
+    table = ctx.alloc_table()   # the symmetric-window table: the P2P fused path bench.py runs
+    table.copy_(synth.table_values(cfg.V, cfg.D, "signed", device=dev))
 else:
     flags = (0 if os.environ.get("TRACE_NO_EVENTS") else lmscale.FLAG_TIMING) | \
         (lmscale.FLAG_GRAPH if os.environ.get("TRACE_GRAPH") else 0)
