@@ -19,6 +19,7 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -326,6 +327,9 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
                                          /*multimem=*/true);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  // the peers' generic-proxy stores of M_g, now acquired, are read below by
+  // bulk copies (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   nv_stamp(a.trace, 49);
   if (__ldcg(&a.sc3->err) & 1u) return;      // id error on some rank: all ranks leave
   const int64_t Ug = a.sc3->u_global;
@@ -698,7 +702,12 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
       }
       // several CTAs per SM (one CTA's bulk-copy stream saturates below the
       // SM's share: tools/gather_probe.cu)
-      k_p2p_bulk<<<cps * st->ctas, PB_THREADS, smem, s>>>(a);
+      // every CTA resident (the LSA barriers pair CTA k of every rank)
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2p_bulk, PB_THREADS, smem) !=
+              cudaSuccess || occ < 1)
+        occ = 1;
+      k_p2p_bulk<<<std::min(cps, occ) * st->ctas, PB_THREADS, smem, s>>>(a);
     } else if (v4) {
       k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
     } else {
