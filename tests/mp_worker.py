@@ -175,6 +175,38 @@ def run_graph_equals_eager(cfg, rank, G, dev, F=0.0):
         print(f"graph==eager G={G} {cfg.name} F={F}", flush=True)
 
 
+def run_graph_compression_toggle(cfg, rank, G, dev):
+    """with LMSCALE_FLAG_GRAPH, switching compression on after a
+    step was captured must not replay the old (fp32) graph -- the step after
+    the switch runs the compressed exchange and matches the oracle's R15
+    exchange bit for bit (INT mode, F = 1)."""
+    lr = synth.default_lr("int")
+    J = [synth.ids_for(cfg, g) for g in range(G)]
+    Dh = [synth.grad_values(cfg.K, cfg.D, "int", rank=g) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, "int")
+    ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_GRAPH)
+    E = ctx.alloc_table()
+    E.copy_(E0.to(dev))
+    ids = torch.from_numpy(J[rank].view(np.int32)).to(dev)
+    g = Dh[rank].to(dev)
+    ctx.step(ids, g, E, lr)                 # captured without compression
+    torch.cuda.synchronize()
+    assert ctx.stats()["fused_s5_s6"] == 2
+    E.copy_(E0.to(dev))
+    torch.cuda.synchronize()
+    ctx.set_compression(1.0)
+    ctx.step(ids, g, E, lr)                 # same arguments: must re-capture
+    torch.cuda.synchronize()
+    assert ctx.stats()["fused_s5_s6"] == 3
+    Eo = E0.numpy().copy()
+    oracle.sync_unique_compressed(J, [d.numpy() for d in Dh], Eo, lr, 1.0)
+    np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+    check_replicas(E, "graph compression toggle")
+    if rank == 0:
+        print(f"graph compression toggle G={G}", flush=True)
+    ctx.close()
+
+
 def run_compressed_small(cfg, mode, rank, G, dev, F, own_table=False, fmt="fp16"):
     """lmscale_step with compression (Sec. 3.3, R15) against
     oracle.sync_unique_compressed: INT mode bit-exact over the whole table,
@@ -385,6 +417,7 @@ def main():
     if "small" in which or "graph" in which:
         run_graph_equals_eager(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev)
         run_graph_equals_eager(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev, F=1.0)
+        run_graph_compression_toggle(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev)
     if "seed" in which:
         ugs = {p: run_seeded(synth.CONFIGS["tiny"].with_(G=G), rank, G, dev, p, S=512)
                for p in ("distinct", "power", "same")}
