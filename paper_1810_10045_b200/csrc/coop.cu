@@ -11,7 +11,9 @@
 //     token) -- or, with the symmetric window, the OR of the G ranks' local
 //     bitmaps read over NVLink -- then a popcount scan over the bitmap that
 //     emits I^ in ascending order and the per-word rank table, U_g, and the
-//     J^ -> I^ map l2g.
+//     J^ -> I^ map l2g (each CTA maps the local words of its own word range,
+//     found through S1's per-word local prefix lrank).  Peer mode: handshake
+//     + 1 grid barrier; gathered ids: 3.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -75,17 +77,6 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
     }
     grid_barrier(a.bar);
     stamp(a.trace, 33);
-    // phase A': the global presence bitmap = OR of the G local bitmaps
-    for (int64_t w = gtid; w < a.W; w += gthreads) {
-      uint32_t g = 0u;
-#pragma unroll 8
-      for (int j = 0; j < a.world; ++j)
-        g |= __ldcv(reinterpret_cast<const uint32_t*>(a.peer_base[j] + a.lbits_off) + w);
-      a.gbits[w] = g;
-    }
-    stamp(a.trace, 35);
-    grid_barrier(a.bar);
-    stamp(a.trace, 36);
   } else {
   // phase 0: zero the bitmap and scalars
   for (int64_t w = gtid; w < a.W; w += gthreads) a.gbits[w] = 0u;
@@ -144,12 +135,25 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   stamp(a.trace, 36);
   }  // !peer_mode
 
-  // phase B: popcounts of this CTA's word range (one word per thread per round)
+  // phase B: popcounts of this CTA's word range (one word per thread per
+  // round); in peer mode the range's words are formed here first (phase A':
+  // the OR of the G local bitmaps read over NVLink), so no barrier between
   const int64_t per = (a.W + gridDim.x - 1) / gridDim.x;
   const int64_t w0 = (int64_t)blockIdx.x * per;
   const int64_t w1 = min(a.W, w0 + per);
   uint32_t cnt = 0;
-  for (int64_t w = w0 + tid; w < w1; w += CT) cnt += __popc(__ldcg(a.gbits + w));
+  if (a.peer_mode) {
+    for (int64_t w = w0 + tid; w < w1; w += CT) {
+      uint32_t g = 0u;
+#pragma unroll 8
+      for (int j = 0; j < a.world; ++j)
+        g |= __ldcv(reinterpret_cast<const uint32_t*>(a.peer_base[j] + a.lbits_off) + w);
+      a.gbits[w] = g;
+      cnt += __popc(g);
+    }
+  } else {
+    for (int64_t w = w0 + tid; w < w1; w += CT) cnt += __popc(__ldcg(a.gbits + w));
+  }
   const uint32_t cta_tot = block_sum(cnt, s_scan);
   if (tid == 0) a.ctot[blockIdx.x] = cta_tot;
   stamp(a.trace, 37);
@@ -179,19 +183,21 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   }
   stamp(a.trace, 39);
   if (!a.luniq) return;
-  grid_barrier(a.bar);
-  stamp(a.trace, 40);
+  __syncthreads();  // this CTA's wrank words are written
 
-  // phase D: l2g[u] = slot of J^[u] in I^ (S1 of this rank has completed)
+  // phase D: l2g[u] = slot of J^[u] in I^ for the local words of this CTA's
+  // word range -- a contiguous block of u, [lrank[w0], lrank[w1]) (S1's
+  // per-word local prefix) -- from this CTA's own wrank/gbits: no barrier
   const int U = (int)a.sc1->u_local;
-  for (int64_t u = gtid; u < U; u += gthreads) {
-    const uint32_t w = __ldcg(a.luniq + u);
-    int32_t slot = -1;
-    if (w < a.vocab) {
+  if (w0 < w1) {
+    const int u0 = (int)__ldcg(a.lrank + w0);
+    const int u1 = w1 < a.W ? (int)__ldcg(a.lrank + w1) : U;
+    for (int u = u0 + tid; u < u1; u += CT) {
+      const uint32_t w = __ldcg(a.luniq + u);
+      LMS_CHECK(w < a.vocab && (int64_t)(w >> 5) >= w0 && (int64_t)(w >> 5) < w1);
       const uint32_t below = __ldcg(a.gbits + (w >> 5)) & ((1u << (w & 31u)) - 1u);
-      slot = (int32_t)(__ldcg(a.wrank + (w >> 5)) + __popc(below));
+      a.l2g[u] = (int32_t)(__ldcg(a.wrank + (w >> 5)) + __popc(below));
     }
-    a.l2g[u] = slot;
   }
   stamp(a.trace, 41);
 }

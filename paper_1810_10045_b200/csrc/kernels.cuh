@@ -37,6 +37,7 @@ struct S3Args {
   uint32_t* ctot;  // [grid]
   Sc3* sc;
   const uint32_t* luniq;  // nullptr: skip the l2g phase
+  const uint32_t* lrank;  // S1's per-word local prefix (index in J^ of word w's first id)
   const Sc1* sc1;
   int32_t* l2g;
   unsigned long long* trace;

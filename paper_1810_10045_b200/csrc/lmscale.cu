@@ -282,6 +282,7 @@ lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream
   a.ctot = ctx->ctot;
   a.sc = ctx->sc3;
   a.luniq = ctx->luniq;
+  a.lrank = ctx->lrank;
   a.sc1 = ctx->sc1;
   a.l2g = ctx->l2g;
   a.trace = ctx->trace;
