@@ -606,6 +606,7 @@ class Bench:
                  dense else None,
                  "speedup_unique_vs_dense": dense.get("speedup_unique_vs_dense") if dense
                  else None,
+                 "gate_0.8x": dense.get("gate_0.8x") if dense else None,
                  "S5_S6": upd, "gpu_launches_per_step": launches / args.steps}
         if not headline:
             ctx.close()

@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
       a.sc->err = err;
       a.sc->u_global = 0;
     }
+    stamp(a.trace, 40);
     grid_barrier(a.bar);
     stamp(a.trace, 33);
   } else {
@@ -188,15 +189,33 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   // phase D: l2g[u] = slot of J^[u] in I^ for the local words of this CTA's
   // word range -- a contiguous block of u, [lrank[w0], lrank[w1]) (S1's
   // per-word local prefix) -- from this CTA's own wrank/gbits: no barrier
+  // (the Zipf head puts thousands of local words in the first ranges: 8 per
+  // thread per round, loads issued together)
   const int U = (int)a.sc1->u_local;
   if (w0 < w1) {
     const int u0 = (int)__ldcg(a.lrank + w0);
     const int u1 = w1 < a.W ? (int)__ldcg(a.lrank + w1) : U;
-    for (int u = u0 + tid; u < u1; u += CT) {
-      const uint32_t w = __ldcg(a.luniq + u);
-      LMS_CHECK(w < a.vocab && (int64_t)(w >> 5) >= w0 && (int64_t)(w >> 5) < w1);
-      const uint32_t below = __ldcg(a.gbits + (w >> 5)) & ((1u << (w & 31u)) - 1u);
-      a.l2g[u] = (int32_t)(__ldcg(a.wrank + (w >> 5)) + __popc(below));
+    constexpr int DB = 8;
+    for (int ub = u0; ub < u1; ub += CT * DB) {
+      uint32_t w[DB], bits[DB], base[DB];
+#pragma unroll
+      for (int q = 0; q < DB; ++q) {
+        const int u = ub + q * CT + tid;
+        w[q] = u < u1 ? __ldcg(a.luniq + u) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < DB; ++q) {
+        bits[q] = __ldcg(a.gbits + (w[q] >> 5));
+        base[q] = __ldcg(a.wrank + (w[q] >> 5));
+      }
+#pragma unroll
+      for (int q = 0; q < DB; ++q) {
+        const int u = ub + q * CT + tid;
+        if (u < u1) {
+          LMS_CHECK(w[q] < a.vocab && (int64_t)(w[q] >> 5) >= w0 && (int64_t)(w[q] >> 5) < w1);
+          a.l2g[u] = (int32_t)(base[q] + __popc(bits[q] & ((1u << (w[q] & 31u)) - 1u)));
+        }
+      }
     }
   }
   stamp(a.trace, 41);
@@ -318,8 +337,25 @@ cudaError_t launch_s3(const S3Args& a, int num_sms, cudaStream_t s) {
   if (want < 1) want = 1;
   const int64_t cap = (int64_t)num_sms * occ;
   const int grid = (int)(want < cap ? want : cap);
-  k_s3<<<grid, CO_THREADS, 0, s>>>(a);
-  return cudaGetLastError();
+  // Highest launch priority: at G > 1 S4 (no grid barrier) becomes ready on
+  // the side stream at the same moment (both wait only on S1); S3's CTAs
+  // must be dispatched first, or its grid barrier waits for S4's CTAs to
+  // retire and make room (measured: +~15 us at 1b G = 2).
+  static int prio = 1;
+  if (prio > 0) {
+    int least = 0, greatest = 0;
+    prio = cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess ? greatest : 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(CO_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = prio;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_s3, a);
 }
 
 }  // namespace lms

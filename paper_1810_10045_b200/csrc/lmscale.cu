@@ -1000,7 +1000,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     LAUNCHED(1);
     rec(ctx, EV_AR_END, s);  // us_allreduce = the fused S5+S6 kernel
     if (ctx->trace && !ctx->capturing) {
-      cudaStreamSynchronize(s);
+      print_trace(ctx, s);
       unsigned long long t[64];
       cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
       fprintf(stderr,
