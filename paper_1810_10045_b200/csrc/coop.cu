@@ -62,16 +62,22 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
       const uint32_t e = *a.epoch + 1u;
       *a.epoch = e;
       const uint32_t f = 2u * e + (__ldcg(&a.sc1->err) & 1u);
+      // one sys fence, then relaxed stores (the release pattern): a release
+      // store per peer costs a fence each, 2-5 us apiece while S4 saturates
+      // HBM beside this kernel
       __threadfence_system();
+      stamp(a.trace, 42);
       for (int j = 0; j < a.world; ++j)
-        st_release_sys(reinterpret_cast<uint32_t*>(a.peer_base[j] + a.flags_off) + a.rank, f);
+        st_relaxed_sys(reinterpret_cast<uint32_t*>(a.peer_base[j] + a.flags_off) + a.rank, f);
+      stamp(a.trace, 43);
       const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.peer_base[a.rank] + a.flags_off);
       uint32_t err = 0u;
       for (int j = 0; j < a.world; ++j) {
         uint32_t v;
-        while ((int32_t)((v = ld_acquire_sys(mine + j)) - 2u * e) < 0) __nanosleep(64);
+        while ((int32_t)((v = ld_relaxed_sys(mine + j)) - 2u * e) < 0) __nanosleep(64);
         err |= v & 1u;
       }
+      __threadfence_system();  // acquire pattern: the peers' bitmaps are read after this
       a.sc->err = err;
       a.sc->u_global = 0;
     }

@@ -303,7 +303,7 @@ void print_trace(lmscale_ctx* ctx, cudaStream_t s) {
   for (int i = 1; i <= 22; ++i)
     if (t[i] && t[i - 1]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[0]) * 1e-3);
   fprintf(stderr, " | S3:");
-  for (int i = 33; i <= 41; ++i)
+  for (int i = 33; i <= 43; ++i)
     if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
   if (t[32] > t[0]) fprintf(stderr, " | S1start->S3start %.2f us", (t[32] - t[0]) * 1e-3);
   if (t[54] && t[58]) {
@@ -874,6 +874,11 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   const uint32_t* I = ids;
   int64_t n = k;
   const bool peer_s3 = G > 1 && ctx->peer_s3;
+  // S4 at world 1 with a table: S6 folded in (finished rows go straight into
+  // the table; M is not written and not re-read).  LMSCALE_NO_INLINE_S6:
+  // separate k_update.
+  static const bool no_inline = getenv("LMSCALE_NO_INLINE_S6") != nullptr;
+  const bool inline_s6 = G == 1 && table && !no_inline;
   // compressed exchange (R15): S4 writes binary16 rows, present rows only
   const bool comp = G > 1 && ctx->cF > 0.f;
   // the peer-to-peer fused kernels load only present rows: no zero-fill of M
@@ -971,11 +976,8 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
     LAUNCHED(1);
     ctx->gcounts_valid = true;
   }
-  // S4: segmented scatter-add into M.  World 1: S6
-  // folded in (finished rows go straight into the table; M is not written
-  // and not re-read).  LMSCALE_NO_INLINE_S6: separate k_update.
-  static const bool no_inline = getenv("LMSCALE_NO_INLINE_S6") != nullptr;
-  const bool inline_s6 = G == 1 && table && !no_inline;
+  // S4: segmented scatter-add into M; world 1: S6
+  // folded in (inline_s6 above).
   if (overlap) {
     CK(cudaStreamWaitEvent(s, ctx->ev_s4, 0));  // S4 ran beside S3
   } else {
@@ -1005,9 +1007,14 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
       cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
       fprintf(stderr,
               "[lmscale trace rank %d] S5+S6: barrier1 %.2f  exchange+update %.2f  barrier2 %.2f"
-              "  tail %.2f us | S3 start -> S5+S6 start %.2f us\n",
+              "  tail %.2f us | setup %.2f presence(CTA0) %.2f | S3 start -> S5+S6 start %.2f us | presence table done (last CTA)"
+              " %.2f, exchange done (last CTA) %.2f us after barrier1\n",
               ctx->cfg.rank, (t[49] - t[48]) * 1e-3, (t[50] - t[49]) * 1e-3,
-              (t[51] - t[50]) * 1e-3, (t[52] - t[51]) * 1e-3, (t[48] - t[32]) * 1e-3);
+              (t[51] - t[50]) * 1e-3, (t[52] - t[51]) * 1e-3,
+              t[44] ? (t[44] - t[48]) * 1e-3 : 0.0, t[45] ? (t[45] - t[44]) * 1e-3 : 0.0,
+              (t[48] - t[32]) * 1e-3,
+              t[47] ? ((long long)t[47] - (long long)t[49]) * 1e-3 : 0.0,
+              t[53] ? ((long long)t[53] - (long long)t[49]) * 1e-3 : 0.0);
     }
     rec(ctx, EV_UPD_BEGIN, s);
     rec(ctx, EV_UPD_END, s);

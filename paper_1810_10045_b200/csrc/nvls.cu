@@ -103,6 +103,14 @@ __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
     tr[i] = t;
   }
 }
+// latest over the CTAs (trace slot reset by the host before the step)
+__device__ __forceinline__ void nv_stamp_max(unsigned long long* tr, int i) {
+  if (tr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(tr + i, t);
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a) {
@@ -323,15 +331,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
     fence_mbar_init();
   }
   nv_stamp(a.trace, 48);
-  ncclCoopCta cta;
-  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
-                                         /*multimem=*/true);
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
-  // the peers' generic-proxy stores of M_g, now acquired, are read below by
-  // bulk copies (async proxy)
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  nv_stamp(a.trace, 49);
-  if (__ldcg(&a.sc3->err) & 1u) return;      // id error on some rank: all ranks leave
+  const bool err = __ldcg(&a.sc3->err) & 1u;  // id error on some rank (OR over ranks)
   const int64_t Ug = a.sc3->u_global;
   const int64_t T = Ug > a.rank ? (Ug - a.rank + G - 1) / G : 0;  // this rank's rows
   // this CTA's rows: t = blockIdx.x + i * gridDim.x (interleaved: the Zipf head
@@ -342,23 +342,36 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   const int D = a.D;
   const int ncb = (D + PB_CB - 1) / PB_CB;
   const int lane = tid & 31;
-  int it0 = 0;  // items issued / consumed before this batch (ring phase continuity)
-  for (int64_t b0 = 0; b0 < nmine; b0 += PB_MAXROWS) {
-    const int nrows = (int)(nmine - b0 < PB_MAXROWS ? nmine - b0 : PB_MAXROWS);
-    // ---- presence and row of word I^[r] on every rank, for the batch's rows
+  const uint32_t* pbits[MAXG];
+  const uint32_t* prank[MAXG];
+#pragma unroll
+  for (int j = 0; j < MAXG; ++j) {
+    const char* base = j < G ? reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    pbits[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
+    prank[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
+  }
+  // ---- presence and row of word I^[r] on every rank, for a batch of rows:
+  // the G ranks' presence bitmaps and per-word local prefixes, all of a row's
+  // loads issued together (a chain of 2G remote loads per row cost 12 us at
+  // 1b G = 2)
+  auto presence = [&](int64_t b0, int nrows) {
     for (int i = tid; i < nrows; i += blockDim.x) {
       const int64_t r = a.rank + (int64_t)G * ((int64_t)blockIdx.x + (b0 + i) * nb);
       const uint32_t w = __ldg(a.ihat + r);
+      uint32_t bw[MAXG], lw[MAXG];
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        bw[j] = j < G ? __ldcg(pbits[j] + (w >> 5)) : 0u;
+        lw[j] = (j < G && a.local_m) ? __ldcg(prank[j] + (w >> 5)) : 0u;
+      }
       uint32_t has = 0;
-      for (int j = 0; j < G; ++j) {
-        const char* base = reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j));
-        const uint32_t bits =
-            __ldcv(reinterpret_cast<const uint32_t*>(base + a.lbits_off) + (w >> 5));
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if (j >= G) break;
+        const uint32_t bits = bw[j];
         has |= ((bits >> (w & 31u)) & 1u) << j;
         uint32_t lrow = (uint32_t)r;
-        if (a.local_m)
-          lrow = __ldcv(reinterpret_cast<const uint32_t*>(base + a.lrank_off) + (w >> 5)) +
-                 __popc(bits & ((1u << (w & 31u)) - 1u));
+        if (a.local_m) lrow = lw[j] + __popc(bits & ((1u << (w & 31u)) - 1u));
         LMS_CHECK(lrow < (uint32_t)a.mcap);
         s_lrow[i * G + j] = lrow;
       }
@@ -366,7 +379,29 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
       s_w[i] = w;
       s_has[i] = (uint8_t)has;
     }
+  };
+  // In the local-slot layout (peer S3) every rank's S1 -- the bitmaps and
+  // prefixes read here -- completed before S3's handshake, so the first
+  // batch's table is built while the barrier waits for the peers' S4.
+  const bool early = a.local_m && !err;
+  nv_stamp(a.trace, 44);
+  if (early) presence(0, (int)(nmine < PB_MAXROWS ? nmine : PB_MAXROWS));
+  nv_stamp(a.trace, 45);
+  ncclCoopCta cta;
+  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
+                                         /*multimem=*/true);
+  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  // the peers' generic-proxy stores of M_g, now acquired, are read below by
+  // bulk copies (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  nv_stamp(a.trace, 49);
+  if (err) return;  // all ranks leave, no table row is touched
+  int it0 = 0;  // items issued / consumed before this batch (ring phase continuity)
+  for (int64_t b0 = 0; b0 < nmine; b0 += PB_MAXROWS) {
+    const int nrows = (int)(nmine - b0 < PB_MAXROWS ? nmine - b0 : PB_MAXROWS);
+    if (b0 > 0 || !early) presence(b0, nrows);
     __syncthreads();
+    if (b0 == 0) nv_stamp_max(a.trace, 47);
     const int items = nrows * ncb;
     if (tid >= nct) {
       // -------------------------------------------------------- producer warp
@@ -426,6 +461,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
     __syncthreads();  // the batch's presence table is no longer read
   }
   nv_stamp(a.trace, 50);
+  nv_stamp_max(a.trace, 53);
   bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
   nv_stamp(a.trace, 51);
   nv_stamp(a.trace, 52);

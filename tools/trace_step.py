@@ -39,6 +39,9 @@ else:
         (lmscale.FLAG_GRAPH if os.environ.get("TRACE_GRAPH") else 0)
     ctx = lmscale.Context(cfg.V, cfg.K, cfg.D, flags=flags)
 for i in range(steps):
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()   # ranks enter the step together (eager launches skew them otherwise)
     ctx.step(ids, grad, table, 0.1)
     torch.cuda.synchronize()
     st = ctx.stats()
