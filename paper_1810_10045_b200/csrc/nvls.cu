@@ -92,6 +92,7 @@ struct NvlsKernelArgs {
   size_t lrank_off;   // local-slot layout: byte offset of lrank in the window
   int local_m;        // 1: M_j rows are at rank j's local index (lrank + popcount), else at r
   int pb_slots;       // k_p2p_bulk: shared-memory ring slots
+  int pb_rows;        // k_p2p_bulk: rows per presence-table batch (<= PB_MAXROWS)
   int64_t mcap;       // rows of every rank's M (bounds of the checked build)
   uint32_t vocab;
 };
@@ -385,7 +386,8 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   // batch's table is built while the barrier waits for the peers' S4.
   const bool early = a.local_m && !err;
   nv_stamp(a.trace, 44);
-  if (early) presence(0, (int)(nmine < PB_MAXROWS ? nmine : PB_MAXROWS));
+  const int BR = a.pb_rows;
+  if (early) presence(0, (int)(nmine < BR ? nmine : BR));
   nv_stamp(a.trace, 45);
   ncclCoopCta cta;
   ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
@@ -397,8 +399,8 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   nv_stamp(a.trace, 49);
   if (err) return;  // all ranks leave, no table row is touched
   int it0 = 0;  // items issued / consumed before this batch (ring phase continuity)
-  for (int64_t b0 = 0; b0 < nmine; b0 += PB_MAXROWS) {
-    const int nrows = (int)(nmine - b0 < PB_MAXROWS ? nmine - b0 : PB_MAXROWS);
+  for (int64_t b0 = 0; b0 < nmine; b0 += BR) {
+    const int nrows = (int)(nmine - b0 < BR ? nmine - b0 : BR);
     if (b0 > 0 || !early) presence(b0, nrows);
     __syncthreads();
     if (b0 == 0) nv_stamp_max(a.trace, 47);
@@ -723,10 +725,19 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
       // ring: (G + 1) x 2 KB per slot; the rest of the CTA's share of shared
       // memory after the presence table
       const size_t sb = (size_t)(world + 1) * PB_CB * 4;
-      const size_t lrow_bytes = 4 * (size_t)PB_MAXROWS * world;
       static const int cps_env =
           getenv("LMSCALE_P2P_CTAS_PER_SM") ? atoi(getenv("LMSCALE_P2P_CTAS_PER_SM")) : 0;
       const int cps = cps_env >= 1 && cps_env <= PB_MAX_CPS ? cps_env : 4;  // measured best (tools/ab_p2p.sh)
+      // presence-table batch: this rank's most rows per CTA (U_g <= mcap), so
+      // one batch normally covers them, and the table leaves room for slots
+      static const int rows_env =
+          getenv("LMSCALE_P2P_BATCH_ROWS") ? atoi(getenv("LMSCALE_P2P_BATCH_ROWS")) : 0;
+      int64_t br = rows_env > 0 ? rows_env
+                                : (mcap / world + (int64_t)cps * st->ctas - 1) / ((int64_t)cps * st->ctas);
+      br = (br + 31) / 32 * 32;
+      br = br < 32 ? 32 : br > PB_MAXROWS ? PB_MAXROWS : br;
+      a.pb_rows = (int)br;
+      const size_t lrow_bytes = 4 * (size_t)br * world;
       int slots = (int)(((size_t)200 * 1024 / cps - lrow_bytes) / sb);
       slots = slots < 2 ? 2 : slots > PB_MAXSLOTS ? PB_MAXSLOTS : slots;
       a.pb_slots = slots;
