@@ -231,6 +231,29 @@ LMSCALE_API lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, c
                                         int64_t k, float* table, float lr,
                                         int64_t* num_unique_out /* host, or NULL */, void* stream);
 
+/* The world-G step of lmscale_step on ONE GPU, for validating
+ * the G > 1 kernels without G GPUs: ctxs[r] (host array, r < world, 2 <=
+ * world <= 8) are NO_COMM contexts of rank r of `world` on the same device,
+ * with equal vocab, dim, max_tokens and compression setting; ids[r] (k
+ * uint32), grads[r] (k x dim fp32) and tables[r] (rank r's replica of E,
+ * vocab x dim, updated in place) are device pointers in host arrays.  Runs
+ * the kernels of lmscale_step's P2P path -- S1 on every rank; S3 as the
+ * J^-set exchange (each rank ORs the G presence bitmaps, reading the other
+ * contexts' windows); S4 in the local-slot layout; the fused S5+S6 kernel of
+ * every rank (compressed, Sec. 3.3: both phases of the codec exchange),
+ * reading the peers' M rows and storing each updated row into every replica
+ * -- with the NCCL window replaced by the contexts' buffers and the
+ * cross-rank barriers by launch order (every S1 before any S3, every S4
+ * before any exchange, every compressed phase 1 before any phase 2).
+ * Synchronises `stream`.  Errors: INVALID_ARG (mismatched contexts, NULL
+ * pointers, k out of range), ID_RANGE (an id >= vocab on any rank: no
+ * replica is touched), CUDA. */
+LMSCALE_API lmscale_status lmscale_emulate_step(lmscale_ctx* const* ctxs /* host */, int world,
+                                                const uint32_t* const* ids /* host array */,
+                                                const float* const* grads /* host array */,
+                                                int64_t k, float* const* tables /* host array */,
+                                                float lr, void* stream);
+
 /* S0, the comparison path: all-gather ids and the k x dim grad
  * rows of every rank (Theta(G K D) bytes), then apply all G*k row updates
  * table[I[q]] -= lr * Delta_all[q] with 128-bit vector atomics (the paper's
@@ -287,7 +310,8 @@ LMSCALE_API lmscale_status lmscale_set_timing(lmscale_ctx* ctx, int mode);
  *     own table: E[I^[r]] = fma(-lr, M^[r], E[I^[r]]).
  * Half the NVLink bytes of the fp32 exchange; replicas stay bit-identical.
  * F == 0 turns compression off.  F < 0 or non-finite: INVALID_ARG.  world > 1
- * needs the symmetric window (stats.nvls_available == 1), else UNSUPPORTED.
+ * needs the symmetric window (stats.nvls_available == 1), else UNSUPPORTED
+ * (NO_COMM contexts accept F: it applies to lmscale_emulate_step).
  * world == 1 has no communication and is unaffected.  While compression is
  * on, lmscale_sync_embedding_grad (fp32 M^ rows through NCCL) returns
  * UNSUPPORTED. */

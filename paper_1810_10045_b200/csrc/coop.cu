@@ -53,7 +53,16 @@ __global__ void __launch_bounds__(CO_THREADS, 1) k_s3(S3Args a) {
   const int64_t gthreads = (int64_t)gridDim.x * CT;
 
   stamp(a.trace, 32);
-  if (a.peer_mode) {
+  if (a.peer_mode == 2) {
+    // emulation: every rank's S1 completed before this launch
+    if (gtid == 0) {
+      uint32_t err = 0u;
+      for (int j = 0; j < a.world; ++j) err |= __ldcg(&a.peer_sc1[j]->err) & 1u;
+      a.sc->err = err;
+      a.sc->u_global = 0;
+    }
+    grid_barrier(a.bar);
+  } else if (a.peer_mode) {
     // handshake: this rank's S1 (the previous kernel on this stream) is
     // complete; tell every peer, then wait until every peer has said so
     // (flag = 2 * epoch + this rank's id-error bit: every rank learns every

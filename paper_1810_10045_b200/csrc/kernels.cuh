@@ -45,9 +45,11 @@ struct S3Args {
   // peer mode (the J^-set exchange): instead of building
   // the bitmap from a gathered I, OR the G local presence bitmaps (S1's lbits)
   // read from the peers' symmetric windows after a flag handshake
-  int peer_mode;
+  int peer_mode;         // 1: flag handshake; 2: emulation (lmscale_emulate_step:
+                         // every rank's S1 ran before, errors from peer_sc1)
   int world, rank;
   char* peer_base[8];   // LSA base of each rank's M window
+  const Sc1* peer_sc1[8];  // peer_mode 2: each rank's S1 scalars
   size_t lbits_off;     // byte offset of lbits in the window
   size_t flags_off;     // byte offset of the per-rank arrival flags (world words)
   uint32_t* epoch;      // local step counter of the handshake (device)
@@ -192,6 +194,14 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
 bool nvls_use_p2p(int world);
 // LSA base of every rank's M window (world entries written to out_host)
 bool nvls_peer_bases(NvlsState* st, int world, void** out_host);
+// lmscale_emulate_step: rank `rank`'s P2P fused kernel with the peers'
+// M-window bases / tables given directly (G contexts on one GPU, no
+// barriers: launch order).  Compressed (cF > 0): phase 1 or 2.
+cudaError_t launch_p2p_emulated(char* const* m_bases, float* const* tables, int world, int rank,
+                                const uint32_t* ihat, const Sc3* sc3, const float* M, int D,
+                                float lr, size_t lbits_off, size_t lrank_off, size_t mhat_off,
+                                float cF, int cbf, int phase, int64_t mcap, uint32_t vocab,
+                                int num_sms, cudaStream_t s);
 ncclWindow_t nvls_register_table(ncclComm_t comm, void* table, size_t bytes, char* err,
                                  size_t errlen);
 void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w);

@@ -262,13 +262,18 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
 
 // S3 on stream s: one launch (bitmap, scan, I^, U_g,
 // and the l2g map of the last S1, which must be complete on `s`).
+// emu (lmscale_emulate_step): the world's contexts on this GPU; the peers'
+// bitmaps are read from their windows after every rank's S1 (no handshake).
 lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream_t s,
-                      bool peer = false) {
+                      bool peer = false, lmscale_ctx* const* emu = nullptr) {
   S3Args a;
-  a.peer_mode = peer ? 1 : 0;
+  a.peer_mode = emu ? 2 : peer ? 1 : 0;
   a.world = ctx->cfg.world;
   a.rank = ctx->cfg.rank;
-  for (int j = 0; j < 8; ++j) a.peer_base[j] = ctx->peer_base[j];
+  for (int j = 0; j < 8; ++j) {
+    a.peer_base[j] = emu ? (j < a.world ? (char*)emu[j]->M : nullptr) : ctx->peer_base[j];
+    a.peer_sc1[j] = emu && j < a.world ? emu[j]->sc1 : nullptr;
+  }
   a.lbits_off = ctx->lbits_off;
   a.flags_off = ctx->flags_off;
   a.epoch = ctx->s3_epoch;
@@ -289,7 +294,7 @@ lmscale_status run_s3(lmscale_ctx* ctx, const uint32_t* I, int64_t n, cudaStream
   a.bar = ctx->bars + 2;
   CK(launch_s3(a, ctx->num_sms, s));
   LAUNCHED(1);
-  ctx->last_n = peer ? (int64_t)ctx->cfg.world * ctx->last_k : n;  // I has G*k ids either way
+  ctx->last_n = (peer || emu) ? (int64_t)ctx->cfg.world * ctx->last_k : n;  // I has G*k ids either way
   ctx->have_s3 = true;
   return LMSCALE_OK;
 }
@@ -458,8 +463,6 @@ lmscale_status lmscale_set_compression(lmscale_ctx* ctx, float F) {
   if (F > 0.f && comm_enabled(ctx) && !ctx->nvls)
     return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "compression needs the symmetric window: %s",
                 ctx->nvls_why);
-  if (F > 0.f && (ctx->cfg.flags & LMSCALE_FLAG_NO_COMM) && ctx->cfg.world > 1)
-    return fail(ctx, LMSCALE_ERR_UNSUPPORTED, "compression on a NO_COMM context");
   if (F > 0.f && ctx->cfg.world > 8)
     return fail(ctx, LMSCALE_ERR_UNSUPPORTED,
                 "the compressed exchange addresses at most 8 peers (world %d)", ctx->cfg.world);
@@ -597,6 +600,7 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     // ncclMemAlloc and is registered with NCCL (zero-copy NVLS / symmetric use).
     // (+256: room to align the compressed M^ region at byte 2*ucap*D)
     const size_t m_bytes = align_up(4 * (size_t)ctx->ucap * D + 256, 1 << 21);
+    size_t m_bytes_used = m_bytes;
     ctx->mhat_off = align_up(2 * (size_t)ctx->ucap * D, 256);
     size_t o_part = take(4 * (size_t)2 * ctx->nr_max * D);
     size_t o_part2 = take(4 * (size_t)2 * ctx->nr_max * D);
@@ -648,23 +652,25 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
     CK(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
     for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&ctx->tev[i]));
     ctx->tmode = (cfg->flags & LMSCALE_FLAG_TIMING) ? 2 : 0;
+    // M and this rank's local presence bitmap, per-word prefix and counts
+    // share one window: the fused kernel reads the peers' bitmaps to load only
+    // present rows
+    const size_t lb_off = m_bytes;
+    const size_t lr_off = align_up(m_bytes + 4 * (size_t)ctx->W, 256);
+    const size_t ct_off = align_up(lr_off + 4 * (size_t)ctx->W, 256);
+    const size_t fl_off = align_up(ct_off + 4 * (size_t)K, 256);
+    const size_t win_bytes = align_up(fl_off + 4 * 64, 1 << 21);
     if (comm_enabled(ctx)) {
       if (!nccl_id) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "world > 1 needs an NCCL id");
       ncclUniqueId id;
       memcpy(&id, nccl_id, sizeof(id));
       NK(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
-      // M and this rank's local presence bitmap share one symmetric window:
-      // the fused kernel reads the peers' bitmaps to load only present rows
-      const size_t lb_off = m_bytes;
-      const size_t lr_off = align_up(m_bytes + 4 * (size_t)ctx->W, 256);
-      const size_t ct_off = align_up(lr_off + 4 * (size_t)ctx->W, 256);
-      const size_t fl_off = align_up(ct_off + 4 * (size_t)K, 256);
-      const size_t win_bytes = align_up(fl_off + 4 * 64, 1 << 21);
       void* m = nullptr;
       if (ncclMemAlloc(&m, win_bytes) != ncclSuccess)
         return fail(ctx, LMSCALE_ERR_OOM, "ncclMemAlloc(%zu) failed", win_bytes);
       ctx->M = (float*)m;
       ctx->m_nccl = true;
+      m_bytes_used = win_bytes;
       // Fused S5+S6 needs a symmetric window (LSA peer pointers, multicast);
       // without it, M is registered for NCCL's zero-copy all-reduce.
       char why[256] = {0};
@@ -687,14 +693,32 @@ lmscale_status lmscale_init(const lmscale_config* cfg, const uint8_t* nccl_id,
         NK(ncclCommRegister(ctx->comm, ctx->M, win_bytes, &ctx->m_reg));
       }
       CK(cudaMemset(m, 0, win_bytes));
+    } else if (cfg->world > 1) {
+      // NO_COMM at world > 1 (staged calls, lmscale_emulate_step): the same
+      // window layout in device memory, so G contexts on one GPU can stand in
+      // for each other's windows
+      if (cudaMalloc((void**)&ctx->M, win_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(%zu) failed", win_bytes);
+      }
+      char* m = (char*)ctx->M;
+      ctx->lbits = (uint32_t*)(m + lb_off);
+      ctx->lbits_off = lb_off;
+      ctx->flags_off = fl_off;
+      ctx->lrank_off = lr_off;
+      ctx->lrank = (uint32_t*)(m + lr_off);
+      ctx->counts_off = ct_off;
+      ctx->counts = (int32_t*)(m + ct_off);
+      CK(cudaMemset(m, 0, win_bytes));
+      m_bytes_used = win_bytes;
     } else {
       if (cudaMalloc((void**)&ctx->M, m_bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(ctx, LMSCALE_ERR_OOM, "cudaMalloc(%zu) failed", m_bytes);
       }
+      CK(cudaMemset(ctx->M, 0, m_bytes));
     }
-    if (!ctx->m_nccl) CK(cudaMemset(ctx->M, 0, m_bytes));
-    off += m_bytes;
+    off += m_bytes_used;
     if (getenv("LMSCALE_PHASE_TRACE")) {
       CK(cudaMalloc(&ctx->trace, 64 * sizeof(unsigned long long)));
       CK(cudaMemset(ctx->trace, 0, 64 * sizeof(unsigned long long)));
@@ -1119,6 +1143,66 @@ lmscale_status lmscale_sync_embedding_grad(lmscale_ctx* ctx, const uint32_t* ids
                                            lmscale_sparse_grad* out, void* stream) {
   if (ctx && !out) return fail(ctx, LMSCALE_ERR_INVALID_ARG, "out is NULL");
   return step_impl(ctx, ids, grad, k, nullptr, 0.f, true, out, stream);
+}
+
+lmscale_status lmscale_emulate_step(lmscale_ctx* const* ctxs, int world,
+                                    const uint32_t* const* ids, const float* const* grads,
+                                    int64_t k, float* const* tables, float lr, void* stream) {
+  if (!ctxs || !ids || !grads || !tables || world < 2 || world > 8) return LMSCALE_ERR_INVALID_ARG;
+  for (int r = 0; r < world; ++r) {
+    lmscale_ctx* c = ctxs[r];
+    if (!c) return LMSCALE_ERR_INVALID_ARG;
+    if (c->cfg.world != world || c->cfg.rank != r || !(c->cfg.flags & LMSCALE_FLAG_NO_COMM) ||
+        c->cfg.vocab != ctxs[0]->cfg.vocab || c->cfg.dim != ctxs[0]->cfg.dim ||
+        c->cfg.device != ctxs[0]->cfg.device || c->K != ctxs[0]->K || c->cF != ctxs[0]->cF ||
+        c->cbf != ctxs[0]->cbf)
+      return fail(c, LMSCALE_ERR_INVALID_ARG,
+                  "emulate_step: context %d must be a NO_COMM context of rank %d of world %d "
+                  "with the same vocab, dim, max_tokens, device and compression as context 0",
+                  r, r, world);
+    if (!grads[r] || !tables[r])
+      return fail(c, LMSCALE_ERR_INVALID_ARG, "emulate_step: grad / table of rank %d is NULL", r);
+    lmscale_status st0 = check_ids_args(c, ids[r], k);
+    if (st0) return st0;
+  }
+  lmscale_ctx* ctx = ctxs[0];  // errors of the launches are reported on context 0
+  cudaStream_t s = S(stream);
+  const float cF = ctx->cF;
+  const int D = (int)ctx->cfg.dim;
+  for (int r = 0; r < world; ++r) {
+    begin_call(ctxs[r]);
+    ctxs[r]->timing_valid = false;
+  }
+  lmscale_status st = LMSCALE_OK;
+  // S1 on every rank, then S3 (J^-set exchange) and S4 (local-slot layout)
+  for (int r = 0; r < world && !st; ++r) st = run_s1(ctxs[r], ids[r], k, nullptr, s);
+  for (int r = 0; r < world && !st; ++r) st = run_s3(ctxs[r], nullptr, 0, s, true, ctxs);
+  for (int r = 0; r < world && !st; ++r)
+    st = run_s4(ctxs[r], grads[r], s, nullptr, lr, false, cF, false, /*local_slots=*/true);
+  if (st) return st;
+  // S5+S6: every rank's fused kernel (compressed: every phase 1, then every phase 2)
+  char* bases[8];
+  for (int j = 0; j < world; ++j) bases[j] = (char*)ctxs[j]->M;
+  for (int ph = 1; ph <= (cF > 0.f ? 2 : 1); ++ph)
+    for (int r = 0; r < world; ++r) {
+      lmscale_ctx* c = ctxs[r];
+      CK(launch_p2p_emulated(bases, tables, world, r, c->ihat, c->sc3, c->M, D, lr, c->lbits_off,
+                             c->lrank_off, c->mhat_off, cF, c->cbf, ph, c->ucap,
+                             (uint32_t)c->cfg.vocab, c->num_sms, s));
+      c->kernels_call += 1;
+    }
+  for (int r = 0; r < world; ++r) {
+    lmscale_ctx* c = ctxs[r];
+    c->have_s3 = true;
+    c->m_consumed = true;
+    c->lbits_clean = false;
+    end_call(c);
+  }
+  CK(cudaMemcpyAsync(ctx->h_sc3, ctx->sc3, sizeof(Sc3) + sizeof(Sc1), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (ctx->h_sc3->err & 1u)
+    return fail(ctx, LMSCALE_ERR_ID_RANGE, "a token id >= vocab on some rank");
+  return LMSCALE_OK;
 }
 
 lmscale_status lmscale_step(lmscale_ctx* ctx, const uint32_t* ids, const float* grad, int64_t k,

@@ -95,6 +95,45 @@ struct NvlsKernelArgs {
   int pb_rows;        // k_p2p_bulk: rows per presence-table batch (<= PB_MAXROWS)
   int64_t mcap;       // rows of every rank's M (bounds of the checked build)
   uint32_t vocab;
+  // emulation (lmscale_emulate_step): each rank's M-window base and table
+  char* emu_m[8];
+  float* emu_t[8];
+};
+
+// Peer access of the P2P kernels.  Product (EMU = false): the NCCL symmetric
+// windows (LSA pointers over NVLink) and per-CTA-index LSA barriers.
+// Emulation (EMU = true, lmscale_emulate_step): the G ranks are G contexts on
+// one GPU whose kernels run one after the other, the window bases are those
+// contexts' buffers, and the launch order gives what the barriers give (every
+// rank's S4 before any exchange; compressed: every phase 1 before any phase 2).
+template <bool EMU>
+__device__ __forceinline__ char* peer_m(const NvlsKernelArgs& a, int j) {
+  if constexpr (EMU)
+    return a.emu_m[j];
+  else
+    return reinterpret_cast<char*>(ncclGetLsaPointer(a.win, 0, j));
+}
+template <bool EMU>
+__device__ __forceinline__ float* peer_t(const NvlsKernelArgs& a, int j) {
+  if constexpr (EMU)
+    return a.emu_t[j];
+  else
+    return reinterpret_cast<float*>(ncclGetLsaPointer(a.twin, 0, j));
+}
+template <bool EMU>
+struct PeerBar;
+template <>
+struct PeerBar<false> {
+  ncclCoopCta cta;
+  ncclLsaBarrierSession<ncclCoopCta> s;
+  __device__ explicit PeerBar(const NvlsKernelArgs& a)
+      : s(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x, /*multimem=*/true) {}
+  __device__ void sync() { s.sync(cta, cuda::memory_order_acq_rel); }
+};
+template <>
+struct PeerBar<true> {
+  __device__ explicit PeerBar(const NvlsKernelArgs&) {}
+  __device__ void sync() { __syncthreads(); }
 };
 
 __device__ __forceinline__ void nv_stamp(unsigned long long* tr, int i) {
@@ -212,14 +251,12 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_nvls_update(NvlsKernelArgs a)
 // e' = fma(-lr, m, E[I^[r]]) and stores e' into every rank's table window.
 // Per GPU and direction that is (G-1)/G x payload for the loads plus the same
 // for the stores -- 1x at G = 2, where multicast needs (1 + 1/G) = 1.5x.
-template <typename T>
+template <typename T, bool EMU>
 __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) {
   constexpr int W = sizeof(T) / sizeof(float);
   constexpr int MAXG = 8;
-  ncclCoopCta cta;
-  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
-                                         /*multimem=*/true);
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  PeerBar<EMU> bar(a);
+  bar.sync();  // every rank's M_g is complete
   // an id >= vocab on any rank (S3's error bit is the OR over ranks): every
   // rank leaves here, no table row is touched (lmscale_sync semantics)
   if (__ldcg(&a.sc3->err) & 1u) return;
@@ -232,15 +269,14 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
   T* pe[MAXG];
 #pragma unroll
   for (int j = 0; j < MAXG; ++j) {
-    pm[j] = j < a.world ? reinterpret_cast<const T*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
-    pe[j] = j < a.world ? reinterpret_cast<T*>(ncclGetLsaPointer(a.twin, 0, j)) : nullptr;
+    pm[j] = j < a.world ? reinterpret_cast<const T*>(peer_m<EMU>(a, j)) : nullptr;
+    pe[j] = j < a.world ? reinterpret_cast<T*>(peer_t<EMU>(a, j)) : nullptr;
   }
   const uint32_t* pb[MAXG];  // each rank's local presence bitmap (S1's lbits)
   const uint32_t* pr[MAXG];  // each rank's lrank (local-slot layout)
 #pragma unroll
   for (int j = 0; j < MAXG; ++j) {
-    const char* base =
-        j < a.world ? reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    const char* base = j < a.world ? peer_m<EMU>(a, j) : nullptr;
     pb[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
     pr[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
   }
@@ -292,7 +328,7 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update(NvlsKernelArgs a) 
       }
     }
   }
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
+  bar.sync();  // every replica holds every updated row
 }
 
 
@@ -312,6 +348,7 @@ constexpr int PB_THREADS = PB_CB / 4 + 32;
 constexpr int PB_MAXSLOTS = 16;
 constexpr int PB_MAX_CPS = 4;     // k_p2p_bulk CTAs per SM (LSA barrier count)
 
+template <bool EMU>
 __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   constexpr int MAXG = 8;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -347,7 +384,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   const uint32_t* prank[MAXG];
 #pragma unroll
   for (int j = 0; j < MAXG; ++j) {
-    const char* base = j < G ? reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    const char* base = j < G ? peer_m<EMU>(a, j) : nullptr;
     pbits[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
     prank[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
   }
@@ -389,10 +426,8 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   const int BR = a.pb_rows;
   if (early) presence(0, (int)(nmine < BR ? nmine : BR));
   nv_stamp(a.trace, 45);
-  ncclCoopCta cta;
-  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
-                                         /*multimem=*/true);
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's M_g is complete
+  PeerBar<EMU> bar(a);
+  bar.sync();  // every rank's M_g is complete
   // the peers' generic-proxy stores of M_g, now acquired, are read below by
   // bulk copies (async proxy)
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -408,7 +443,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
     if (tid >= nct) {
       // -------------------------------------------------------- producer warp
       const char* pm =
-          (lane < G) ? reinterpret_cast<const char*>(ncclGetLsaPointer(a.win, 0, lane)) : nullptr;
+          (lane < G) ? peer_m<EMU>(a, lane) : nullptr;
       for (int q = 0; q < items; ++q) {
         const int it = it0 + q;
         const int s = it % NS, ph = it / NS;
@@ -436,7 +471,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
       float4* pe[MAXG];
 #pragma unroll
       for (int j = 0; j < MAXG; ++j)
-        pe[j] = j < G ? reinterpret_cast<float4*>(ncclGetLsaPointer(a.twin, 0, j)) : nullptr;
+        pe[j] = j < G ? reinterpret_cast<float4*>(peer_t<EMU>(a, j)) : nullptr;
       const int t = tid;
       for (int q = 0; q < items; ++q) {
         const int it = it0 + q;
@@ -464,7 +499,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
   }
   nv_stamp(a.trace, 50);
   nv_stamp_max(a.trace, 53);
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every replica holds every updated row
+  bar.sync();  // every replica holds every updated row
   nv_stamp(a.trace, 51);
   nv_stamp(a.trace, 52);
 }
@@ -484,15 +519,16 @@ __global__ void __launch_bounds__(PB_THREADS) k_p2p_bulk(NvlsKernelArgs a) {
 //      M^: E[I^[r]] = fma(-lr, dec(M^[r]), E[I^[r]]) -- the same instruction on
 //      the same bits on every rank, so the replicas stay bit-identical.
 // Per GPU and direction: (G-1)/G x (present rows + U_g rows) x 2 bytes x D.
-template <typename T>
+// PH: 0 the product kernel (both phases, LSA barriers); emulation: 1 phase
+// 1 only, 2 phase 2 only (every rank's phase 1 is launched first).
+template <typename T, int PH>
 __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a) {
   constexpr int W = sizeof(T) / sizeof(float);
   using H = typename std::conditional<W == 4, uint2, uint16_t>::type;
   constexpr int MAXG = 8;
-  ncclCoopCta cta;
-  ncclLsaBarrierSession<ncclCoopCta> bar(cta, a.dev, ncclTeamTagLsa{}, blockIdx.x,
-                                         /*multimem=*/true);
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every rank's compressed M_g is complete
+  constexpr bool EMU = PH != 0;
+  PeerBar<EMU> bar(a);
+  bar.sync();  // every rank's compressed M_g is complete
   // an id >= vocab on any rank (S3's error bit is the OR over ranks): every
   // rank leaves here, no table row is touched (lmscale_sync semantics)
   if (__ldcg(&a.sc3->err) & 1u) return;
@@ -508,14 +544,14 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
   const uint32_t* pr[MAXG];
 #pragma unroll
   for (int j = 0; j < MAXG; ++j) {
-    char* base = j < a.world ? reinterpret_cast<char*>(ncclGetLsaPointer(a.win, 0, j)) : nullptr;
+    char* base = j < a.world ? peer_m<EMU>(a, j) : nullptr;
     pm[j] = reinterpret_cast<const H*>(base);
     pq[j] = reinterpret_cast<H*>(base + a.mhat_off);
     pb[j] = reinterpret_cast<const uint32_t*>(base + a.lbits_off);
     pr[j] = reinterpret_cast<const uint32_t*>(base + a.lrank_off);
   }
   T* Eo = reinterpret_cast<T*>(a.table);
-  for (int64_t t = gw; a.rank + a.world * t < Ug; t += nw) {
+  for (int64_t t = gw; PH != 2 && a.rank + a.world * t < Ug; t += nw) {
     const int64_t r = a.rank + a.world * t;
     const uint32_t w = __ldg(a.ihat + r);
     const size_t mrow = (size_t)r * C;
@@ -564,7 +600,8 @@ __global__ void __launch_bounds__(NV_THREADS, 1) k_p2p_update_c(NvlsKernelArgs a
       }
     }
   }
-  bar.sync(cta, cuda::memory_order_acq_rel);  // every compressed row of M^ has landed
+  if (PH == 1) return;
+  if (PH == 0) bar.sync();  // every compressed row of M^ has landed
   const H* Q = reinterpret_cast<const H*>(reinterpret_cast<const char*>(a.M) + a.mhat_off);
   T* E = reinterpret_cast<T*>(a.table);
   // rows in the same (owner, t) order as phase 1: the barrier above is per
@@ -677,6 +714,101 @@ void nvls_deregister_table(ncclComm_t comm, ncclWindow_t w) {
   if (w) ncclCommWindowDeregister(comm, w);
 }
 
+// The P2P fused kernel: k_p2p_bulk (rows staged by bulk copies) when rows
+// are 16-byte vectors, else k_p2p_update (warp loads).
+template <bool EMU>
+void p2p_launch(NvlsKernelArgs& a, int ctas, const float* M, cudaStream_t s) {
+  const int world = a.world;
+  const bool v4 = a.D % 4 == 0 && (uintptr_t)a.table % 16 == 0;
+  static const bool no_bulk = getenv("LMSCALE_NO_P2P_BULK") != nullptr;
+  const bool bulk = v4 && !no_bulk && (uintptr_t)M % 16 == 0;
+  if (!bulk) {
+    if (v4)
+      k_p2p_update<float4, EMU><<<ctas, NV_THREADS, 0, s>>>(a);
+    else
+      k_p2p_update<float, EMU><<<ctas, NV_THREADS, 0, s>>>(a);
+    return;
+  }
+  // ring: (G + 1) x 2 KB per slot; the rest of the CTA's share of shared
+  // memory after the presence table
+  const size_t sb = (size_t)(world + 1) * PB_CB * 4;
+  static const int cps_env =
+      getenv("LMSCALE_P2P_CTAS_PER_SM") ? atoi(getenv("LMSCALE_P2P_CTAS_PER_SM")) : 0;
+  const int cps = cps_env >= 1 && cps_env <= PB_MAX_CPS ? cps_env : 4;  // measured best (tools/ab_p2p.sh)
+  // presence-table batch: this rank's most rows per CTA (U_g <= mcap), so
+  // one batch normally covers them, and the table leaves room for slots
+  static const int rows_env =
+      getenv("LMSCALE_P2P_BATCH_ROWS") ? atoi(getenv("LMSCALE_P2P_BATCH_ROWS")) : 0;
+  int64_t br = rows_env > 0 ? rows_env
+                            : (a.mcap / world + (int64_t)cps * ctas - 1) / ((int64_t)cps * ctas);
+  br = (br + 31) / 32 * 32;
+  br = br < 32 ? 32 : br > PB_MAXROWS ? PB_MAXROWS : br;
+  a.pb_rows = (int)br;
+  const size_t lrow_bytes = 4 * (size_t)br * world;
+  int slots = (int)(((size_t)200 * 1024 / cps - lrow_bytes) / sb);
+  slots = slots < 2 ? 2 : slots > PB_MAXSLOTS ? PB_MAXSLOTS : slots;
+  a.pb_slots = slots;
+  const size_t smem = (size_t)slots * sb + lrow_bytes;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_p2p_bulk<EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  // several CTAs per SM (one CTA's bulk-copy stream saturates below the
+  // SM's share: tools/gather_probe.cu)
+  // every CTA resident (the LSA barriers pair CTA k of every rank)
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2p_bulk<EMU>, PB_THREADS, smem) !=
+          cudaSuccess || occ < 1)
+    occ = 1;
+  k_p2p_bulk<EMU><<<std::min(cps, occ) * ctas, PB_THREADS, smem, s>>>(a);
+}
+
+cudaError_t launch_p2p_emulated(char* const* m_bases, float* const* tables, int world, int rank,
+                                const uint32_t* ihat, const Sc3* sc3, const float* M, int D,
+                                float lr, size_t lbits_off, size_t lrank_off, size_t mhat_off,
+                                float cF, int cbf, int phase, int64_t mcap, uint32_t vocab,
+                                int num_sms, cudaStream_t s) {
+  NvlsKernelArgs a{};
+  a.mcap = mcap;
+  a.vocab = vocab;
+  a.cbf = cbf;
+  a.lrank_off = lrank_off;
+  a.local_m = 1;
+  a.lbits_off = lbits_off;
+  a.cF = cF;
+  a.mhat_off = mhat_off;
+  a.ihat = ihat;
+  a.sc3 = sc3;
+  a.table = tables[rank];
+  a.M = M;
+  a.D = D;
+  a.lr = lr;
+  a.rank = rank;
+  a.world = world;
+  for (int j = 0; j < world && j < 8; ++j) {
+    a.emu_m[j] = m_bases[j];
+    a.emu_t[j] = tables[j];
+  }
+  const bool v4 = D % 4 == 0 && (uintptr_t)a.table % 16 == 0;
+  if (cF > 0.f) {
+    if (phase == 1) {
+      if (v4)
+        k_p2p_update_c<float4, 1><<<num_sms, NV_THREADS, 0, s>>>(a);
+      else
+        k_p2p_update_c<float, 1><<<num_sms, NV_THREADS, 0, s>>>(a);
+    } else {
+      if (v4)
+        k_p2p_update_c<float4, 2><<<num_sms, NV_THREADS, 0, s>>>(a);
+      else
+        k_p2p_update_c<float, 2><<<num_sms, NV_THREADS, 0, s>>>(a);
+    }
+  } else {
+    p2p_launch<true>(a, num_sms, M, s);
+  }
+  return cudaGetLastError();
+}
+
 void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, float* table,
                         const float* M, int D, float lr, int rank, int world,
                         unsigned long long* trace, ncclWindow_t twin, size_t lbits_off,
@@ -708,58 +840,18 @@ void launch_nvls_update(NvlsState* st, const uint32_t* ihat, const Sc3* sc3, flo
   const bool v4 = D % 4 == 0 && (uintptr_t)table % 16 == 0;
   static bool once = (max_carveout((const void*)k_nvls_update<float4>),
                       max_carveout((const void*)k_nvls_update<float>),
-                      max_carveout((const void*)k_p2p_update<float4>),
-                      max_carveout((const void*)k_p2p_update<float>),
-                      max_carveout((const void*)k_p2p_update_c<float4>),
-                      max_carveout((const void*)k_p2p_update_c<float>), true);
+                      max_carveout((const void*)k_p2p_update<float4, false>),
+                      max_carveout((const void*)k_p2p_update<float, false>),
+                      max_carveout((const void*)k_p2p_update_c<float4, 0>),
+                      max_carveout((const void*)k_p2p_update_c<float, 0>), true);
   (void)once;
   if (cF > 0.f) {  // compressed exchange (any table; G <= 8)
     if (v4)
-      k_p2p_update_c<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
+      k_p2p_update_c<float4, 0><<<st->ctas, NV_THREADS, 0, s>>>(a);
     else
-      k_p2p_update_c<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
+      k_p2p_update_c<float, 0><<<st->ctas, NV_THREADS, 0, s>>>(a);
   } else if (twin && nvls_use_p2p(world)) {
-    static const bool no_bulk = getenv("LMSCALE_NO_P2P_BULK") != nullptr;
-    const bool bulk = v4 && !no_bulk && (uintptr_t)M % 16 == 0;
-    if (bulk) {
-      // ring: (G + 1) x 2 KB per slot; the rest of the CTA's share of shared
-      // memory after the presence table
-      const size_t sb = (size_t)(world + 1) * PB_CB * 4;
-      static const int cps_env =
-          getenv("LMSCALE_P2P_CTAS_PER_SM") ? atoi(getenv("LMSCALE_P2P_CTAS_PER_SM")) : 0;
-      const int cps = cps_env >= 1 && cps_env <= PB_MAX_CPS ? cps_env : 4;  // measured best (tools/ab_p2p.sh)
-      // presence-table batch: this rank's most rows per CTA (U_g <= mcap), so
-      // one batch normally covers them, and the table leaves room for slots
-      static const int rows_env =
-          getenv("LMSCALE_P2P_BATCH_ROWS") ? atoi(getenv("LMSCALE_P2P_BATCH_ROWS")) : 0;
-      int64_t br = rows_env > 0 ? rows_env
-                                : (mcap / world + (int64_t)cps * st->ctas - 1) / ((int64_t)cps * st->ctas);
-      br = (br + 31) / 32 * 32;
-      br = br < 32 ? 32 : br > PB_MAXROWS ? PB_MAXROWS : br;
-      a.pb_rows = (int)br;
-      const size_t lrow_bytes = 4 * (size_t)br * world;
-      int slots = (int)(((size_t)200 * 1024 / cps - lrow_bytes) / sb);
-      slots = slots < 2 ? 2 : slots > PB_MAXSLOTS ? PB_MAXSLOTS : slots;
-      a.pb_slots = slots;
-      const size_t smem = (size_t)slots * sb + lrow_bytes;
-      static size_t set = 0;
-      if (smem > set) {
-        cudaFuncSetAttribute(k_p2p_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set = smem;
-      }
-      // several CTAs per SM (one CTA's bulk-copy stream saturates below the
-      // SM's share: tools/gather_probe.cu)
-      // every CTA resident (the LSA barriers pair CTA k of every rank)
-      int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2p_bulk, PB_THREADS, smem) !=
-              cudaSuccess || occ < 1)
-        occ = 1;
-      k_p2p_bulk<<<std::min(cps, occ) * st->ctas, PB_THREADS, smem, s>>>(a);
-    } else if (v4) {
-      k_p2p_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
-    } else {
-      k_p2p_update<float><<<st->ctas, NV_THREADS, 0, s>>>(a);
-    }
+    p2p_launch<false>(a, st->ctas, M, s);
   } else if (v4) {
     k_nvls_update<float4><<<st->ctas, NV_THREADS, 0, s>>>(a);
   } else {

@@ -79,6 +79,9 @@ _sync = _sig("lmscale_sync_embedding_grad", _S,
 _apply = _sig("lmscale_apply_sparse_update", _S,
               [_P, _P, ctypes.POINTER(SparseGradC), ctypes.c_float, _P])
 _step = _sig("lmscale_step", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, ctypes.POINTER(_i64), _P])
+_emulate_step = _sig("lmscale_emulate_step", _S, [ctypes.POINTER(_P), ctypes.c_int,
+                                                  ctypes.POINTER(_P), ctypes.POINTER(_P), _i64,
+                                                  ctypes.POINTER(_P), ctypes.c_float, _P])
 _dense = _sig("lmscale_sync_dense_baseline", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, _P])
 _dense_apply = _sig("lmscale_dense_apply", _S, [_P, _P, _P, _i64, _P, ctypes.c_float, _P])
 _host_step = _sig("lmscale_train_step_host", _S,
@@ -103,7 +106,8 @@ _version = _sig("lmscale_version", ctypes.c_char_p, [])
 EXPORTED = ["lmscale_get_nccl_id", "lmscale_init", "lmscale_destroy", "lmscale_unique",
             "lmscale_global_unique", "lmscale_scatter_expand", "lmscale_get_sparse_grad",
             "lmscale_get_local_maps", "lmscale_sync_embedding_grad",
-            "lmscale_apply_sparse_update", "lmscale_step", "lmscale_sync_dense_baseline",
+            "lmscale_apply_sparse_update", "lmscale_step", "lmscale_emulate_step",
+            "lmscale_sync_dense_baseline",
             "lmscale_dense_apply", "lmscale_train_step_host", "lmscale_set_timing", "lmscale_alloc_table",
             "lmscale_set_compression", "lmscale_set_codec", "lmscale_compress", "lmscale_decompress",
             "lmscale_plan_seeds", "lmscale_draw_samples", "lmscale_lookup", "lmscale_get_stats",
@@ -122,6 +126,25 @@ def plan_seeds(world: int, policy: str = "power", alpha: float = 0.64, master_se
     if st != OK:
         raise LmscaleError(st, f"lmscale_plan_seeds({world}, {policy}, {alpha})")
     return [int(x) for x in seeds], int(n.value)
+
+
+def emulate_step(ctxs, ids, grads, tables, lr, stream=None):
+    """lmscale_emulate_step: the world-G step of lmscale_step on one GPU.
+    ctxs[r] are NO_COMM contexts (world = len(ctxs), rank r); ids[r], grads[r]
+    and tables[r] are rank r's device tensors (tables updated in place)."""
+    G = len(ctxs)
+    assert len(ids) == len(grads) == len(tables) == G
+    ids = [Context._ids(t) for t in ids]
+    k = ids[0].numel()
+    for g, t, i in zip(grads, tables, ids):
+        assert i.numel() == k
+        assert g.dtype == torch.float32 and g.is_cuda and g.is_contiguous()
+        assert t.dtype == torch.float32 and t.is_cuda and t.is_contiguous()
+    arr = lambda xs: (_P * G)(*[_ptr(x) for x in xs])  # noqa: E731
+    hs = (_P * G)(*[c._h for c in ctxs])
+    st = _emulate_step(hs, G, arr(ids), arr(grads), k, arr(tables), float(lr), _stream(stream))
+    if st != OK:
+        raise LmscaleError(st, "lmscale_emulate_step: " + (_last_error(ctxs[0]._h) or b"").decode())
 
 
 class LmscaleError(RuntimeError):
