@@ -310,3 +310,41 @@ def test_emulated_full_size_sampled(lm, name, G, mode, F):
                        "signed", f"{name} G={G} word {w}")
     close(ctxs)
     del tables, E0
+
+
+@pytest.mark.parametrize("policy", ["power", "same", "distinct"])
+def test_emulated_seeded_output_exchange(lm, policy):
+    """Sec. 3.2 (R16) on the device path at G = 4: every rank draws
+    S candidates with its group's seed (lmscale_plan_seeds +
+    lmscale_draw_samples) into the tail of [K targets || S samples], then the
+    world-G step; against the oracle's plan, draws and steps 1-7 over every
+    rank's list (INT mode, bit-exact; replicas bit-identical)."""
+    G, S, step, mode = 4, 1024, 3, "int"
+    cfg = synth.CONFIGS["tiny"].with_(G=G)
+    lr = synth.default_lr(mode)
+    seeds, ngroups = lm.plan_seeds(G, policy, 0.64, master_seed=181010045)
+    oseeds, on = oracle.plan_seeds(G, policy, alpha=0.64, master_seed=181010045)
+    assert (seeds, ngroups) == (oseeds, on)
+    ctxs = [lm.Context(cfg.V, cfg.K + S, cfg.D, world=G, rank=r, flags=lm.FLAG_NO_COMM)
+            for r in range(G)]
+    ids = []
+    for r in range(G):
+        t = torch.empty(cfg.K + S, dtype=torch.int32, device=dev())
+        t[:cfg.K] = ids_dev(synth.ids_for(cfg, r))
+        ctxs[r].draw_samples(seeds[r], step, S, out=t[cfg.K:])
+        ids.append(t)
+    Dl = [synth.grad_values(cfg.K + S, cfg.D, mode, rank=g) for g in range(G)]
+    E0 = synth.table_values(cfg.V, cfg.D, mode, device=dev())
+    tables = [E0.clone() for _ in range(G)]
+    lm.emulate_step(ctxs, ids, [d.to(dev()) for d in Dl], tables, lr)
+    torch.cuda.synchronize()
+    Jall = [np.concatenate([synth.ids_for(cfg, g), oracle.draw_samples(oseeds[g], step, S, cfg.V)])
+            for g in range(G)]
+    for r in range(G):
+        np.testing.assert_array_equal(ids[r].cpu().numpy().view(np.uint32), Jall[r])
+    Eo = E0.cpu().numpy().copy()
+    ref = oracle.sync_unique(Jall, [d.numpy() for d in Dl], Eo, lr)
+    np.testing.assert_array_equal(tables[0].cpu().numpy(), Eo)
+    check_replicas(tables, f"seeded {policy}")
+    assert ctxs[0].sparse_grad().num_unique == ref["Ug"]
+    close(ctxs)
