@@ -371,8 +371,8 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
       bits[k] = 0u;
       base[k] = 0u;
       if (id[k] < a.vocab) {
-        bits[k] = __ldcg(a.lbits + (id[k] >> 5));
-        base[k] = __ldcg(a.lrank + (id[k] >> 5));
+        bits[k] = __ldca(a.lbits + (id[k] >> 5));
+        base[k] = __ldca(a.lrank + (id[k] >> 5));
       }
     }
 #pragma unroll
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     for (int k = 0; k < TPT; ++k) {
       const int i = tid + k * GT;
       if (i < n && id[k] < a.vocab) {
-        const uint32_t spos = (uint32_t)__ldcg(a.lstart + base[k]) + t[k];
+        const uint32_t spos = (uint32_t)__ldca(a.lstart + base[k]) + t[k];
         LMS_CHECK(spos < (uint32_t)a.K && spos / a.seg_len <= (uint32_t)a.nr);
         a.perm[spos] = sub + i;
         // the S4 range starting here begins inside run u
