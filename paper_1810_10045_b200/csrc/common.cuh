@@ -162,17 +162,30 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
                : "memory");
   return old;
 }
+// Arrival: atom.inc with wrap-around (the last arriver's increment returns
+// the count to 0, no separate reset store) and release semantics; the last
+// arriver (acquire: every arrival is in the count's release sequence) bumps
+// gen with a release store; the others poll gen with relaxed loads and
+// acquire once after the loop.  (An acquire load per poll and a reset store
+// before the release left ~2.2 us between the last arrival and the others
+// passing.)
 __device__ __forceinline__ void grid_barrier(GridBar* b) {
   __syncthreads();  // the CTA's writes happen-before thread 0's release below
   if (threadIdx.x == 0) {
     const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
-    const uint32_t gen = ld_acquire(&b->gen);
-    if (atom_add_acq_rel(&b->count, 1u) == nb - 1) {
-      b->count = 0u;                 // ordered before the release of gen
+    uint32_t gen;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(&b->gen) : "memory");
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(&b->count), "r"(nb - 1u) : "memory");
+    if (old == nb - 1u) {
       st_release(&b->gen, gen + 1u);
     } else {
-      while (ld_acquire(&b->gen) == gen) {
-      }
+      uint32_t g;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&b->gen) : "memory");
+      } while (g == gen);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
   }
   __syncthreads();  // thread 0's acquire happens-before the CTA's reads

@@ -55,6 +55,16 @@ __device__ __forceinline__ void gstamp(unsigned long long* tr, int i) {
   }
 }
 
+// latest over the CTAs of a phase end (slot i), and (slot i + 3) the CTA that
+// set it (diagnostic; racy between near-equal times)
+__device__ __forceinline__ void gstamp_last(unsigned long long* tr, int i) {
+  if (tr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (atomicMax(tr + i, t) < t) tr[i + 3] = blockIdx.x;
+  }
+}
+
 // Block-wide exclusive scan of (a, b) pairs; totals returned through *ta, *tb.
 __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t& ea, uint32_t& eb,
                                             uint32_t& ta, uint32_t& tb, uint32_t* s_a,
@@ -233,6 +243,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     if (a.sc3) atomicOr(&a.sc3->err, 1u);
   }
   gstamp(a.trace, 1);
+  gstamp_last(a.trace, 16);
   grid_barrier(a.bar);
   gstamp(a.trace, 2);
 
@@ -349,6 +360,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     }
   }
   gstamp(a.trace, 3);
+  gstamp_last(a.trace, 17);
   grid_barrier(a.bar);
   gstamp(a.trace, 4);
   if (tid < NST) {  // this range's totals return to zero for the next launch
@@ -400,6 +412,7 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     }
   }
   gstamp(a.trace, 5);
+  gstamp_last(a.trace, 18);
 }
 
 constexpr size_t G1_SMEM = std::max<size_t>(4 * (2 * HS + 2 * G1_MAX_GRID),

@@ -305,8 +305,12 @@ void print_trace(lmscale_ctx* ctx, cudaStream_t s) {
   unsigned long long t[64];
   cudaMemcpy(t, ctx->trace, sizeof(t), cudaMemcpyDeviceToHost);
   fprintf(stderr, "[lmscale trace] S1:");
-  for (int i = 1; i <= 22; ++i)
+  for (int i = 1; i <= 13; ++i)
     if (t[i] && t[i - 1]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[0]) * 1e-3);
+  if (t[16] > t[0])
+    fprintf(stderr, " | last CTA: PA end %.2f (cta %llu) PC end %.2f (cta %llu) PD end %.2f (cta %llu)",
+            (t[16] - t[0]) * 1e-3, t[19], (t[17] - t[0]) * 1e-3, t[20], (t[18] - t[0]) * 1e-3,
+            t[21]);
   fprintf(stderr, " | S3:");
   for (int i = 33; i <= 43; ++i)
     if (t[i] && t[32]) fprintf(stderr, " %d:%.2f", i, (t[i] - t[32]) * 1e-3);
