@@ -25,6 +25,7 @@ cols = [w for w in want if w in hdr]
 if as_csv:
     w = csv.writer(sys.stdout)
     w.writerow(["Kernel Name"] + cols)
+    w.writerow(["(unit)"] + [rows[1][hdr.index(c)] for c in cols])
     for r in rows[2:]:
         w.writerow([r[hdr.index('Kernel Name')]] + [r[hdr.index(c)] for c in cols])
 else:
