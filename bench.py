@@ -205,6 +205,68 @@ def oracle_sample(cfg, G, mode, seconds, threads=1, inputs=None):
     return tps, desc, n, dt
 
 
+ORACLE_MEM_BUDGET = 12 << 30   # host bytes one whole-width oracle step may hold
+
+
+def oracle_step_bytes(cfg, G, Dc):
+    """Host bytes of one oracle step (sync_unique) over Dc columns: the G
+    inputs, the G fp64 M_g (U_g x Dc), M^, the G fp64 local sums and E."""
+    import synth
+    ug = min(synth.expected_unique(cfg.V, cfg.s, G * cfg.K) * 1.05, cfg.V)
+    ui = min(synth.expected_unique(cfg.V, cfg.s, cfg.K) * 1.05, cfg.V)
+    return int(Dc * (G * cfg.K * 4 + (G + 1) * ug * 8 + G * ui * 8 + cfg.V * 4))
+
+
+def oracle_inputs_cols(cfg, G, mode, Dc):
+    """Ids of the G ranks and Dc-column gradient blocks (the same seeded
+    value distribution; the oracle's work does not depend on the values)."""
+    import synth
+    return ([synth.ids_for(cfg, g) for g in range(G)],
+            [synth.grad_values(cfg.K, Dc, mode, rank=g).numpy() for g in range(G)])
+
+
+def oracle_sample_cols(cfg, G, mode, seconds, Dc, inputs):
+    """The oracle on a workload too large for host memory in whole-width
+    steps: the same functions in sync_unique's order, with the
+    id steps (1, 3, 4 and the remap) on the full streams and the value steps
+    (2, 5, 6, 7 -- column-separable, the same work per column) on a Dc-column
+    block; a step's time = t_ids + (D / Dc) t_values."""
+    import oracle
+    import synth
+    J, Dl = inputs
+    E = np.zeros((cfg.V, Dc), np.float32)
+    lr = synth.default_lr(mode)
+    t_ids = t_val = 0.0
+    n = 0
+    while True:
+        t0 = time.perf_counter()
+        ranks = [oracle.unique_local(J[g]) for g in range(G)]            # step 1
+        I = oracle.allgather_ids(J)                                      # step 3
+        Ihat, _ = oracle.unique_global(I)                                # step 4
+        l2g = [oracle.remap(Jh, Ihat, inv)[0] for Jh, _, inv in ranks]
+        t1 = time.perf_counter()
+        Ms = []
+        for g, (Jh, _, inv) in enumerate(ranks):
+            dhat = oracle.reduce_local(Dl[g], inv, Jh.size)               # step 2
+            Ms.append(oracle.scatter_expand(dhat, l2g[g], Ihat.size))    # step 5
+        Mhat64 = oracle.allreduce_sum(Ms)                                # step 6
+        oracle.update_rows(E, Ihat, Mhat64, lr)                          # step 7
+        t2 = time.perf_counter()
+        del Ms, Mhat64
+        t_ids += t1 - t0
+        t_val += t2 - t1
+        n += 1
+        if t_ids + t_val >= seconds or n >= 1000:
+            break
+    step = (t_ids + (cfg.D / Dc) * t_val) / n
+    desc = (f"{n} oracle steps of workload {cfg.name} (G={G} simulated ranks x K={cfg.K} tokens, "
+            f"D={cfg.D}): id steps on the full streams, value steps on a {Dc}-column block "
+            f"scaled by D/{Dc} (a whole-width step needs "
+            f"{oracle_step_bytes(cfg, G, cfg.D) / 2**30:.0f} GiB of host memory); "
+            f"single-threaded C, fp64 accumulation; CPU {cpu_model()}")
+    return G * cfg.K / step, desc, n, t_ids + t_val
+
+
 def config_dict(cfg, args, world):
     return {"workload": cfg.name, "V": cfg.V, "K_per_gpu": cfg.K, "D": cfg.D, "zipf_s": cfg.s,
             "G": world, "value_mode": args.mode, "global_tokens": world * cfg.K,
@@ -226,11 +288,20 @@ def run_reference(args, cfg, rank, world):
         return
     per_step = max(1.0, min(20.0, 90.0 / max(1, args.steps + args.warmup)))
     import synth
-    inputs = ([synth.ids_for(cfg, g) for g in range(world)],
-              [synth.grad_values(cfg.K, cfg.D, args.mode, rank=g).numpy() for g in range(world)])
+    Dc = cfg.D
+    while Dc > 8 and oracle_step_bytes(cfg, world, Dc) > ORACLE_MEM_BUDGET:
+        Dc //= 2
+    if Dc == cfg.D:
+        inputs = ([synth.ids_for(cfg, g) for g in range(world)],
+                  [synth.grad_values(cfg.K, cfg.D, args.mode, rank=g).numpy() for g in range(world)])
+    else:
+        inputs = oracle_inputs_cols(cfg, world, args.mode, Dc)
     times, descs = [], []
     for i in range(args.warmup + args.steps):
-        tps, desc, n, dt = oracle_sample(cfg, world, args.mode, per_step, inputs=inputs)
+        if Dc != cfg.D:
+            tps, desc, n, dt = oracle_sample_cols(cfg, world, args.mode, per_step, Dc, inputs)
+        else:
+            tps, desc, n, dt = oracle_sample(cfg, world, args.mode, per_step, inputs=inputs)
         if i >= args.warmup:
             times.append(tps)
             descs.append(desc)
