@@ -36,6 +36,10 @@ METRIC = "emb-grad sync µs/step & tokens/s at 1/2/4/8 B200; HBM GB/s vs peak"
 UNIT = "tokens/s"
 NVLINK_NOMINAL = 900.0   # GB/s per direction per GPU (north_star's roofline)
 NVLINK_MEASURED = 770.0  # GB/s peer copy per direction (B200_PROFILING.md)
+# GB/s per direction of SM-initiated traffic mixing bulk-copy pulls and SM
+# stores into the peer, both GPUs active (tools/p2p_probe.cu,
+# profiles/r02/g2_nvlink_ceiling_probe.txt): the fused kernel's own pattern
+NVLINK_SM_MIX = 699.0
 
 
 def parse():
@@ -647,6 +651,7 @@ class Bench:
                    "measured_in": "third timed pass, two events bracketing the fused kernel"}
             upd["frac"] = upd["achieved"] / NVLINK_NOMINAL
             upd["frac_of_measured_peer_copy"] = upd["achieved"] / NVLINK_MEASURED
+            upd["frac_of_sm_pattern_ceiling"] = upd["achieved"] / NVLINK_SM_MIX
 
         # ---- dense comparison path (S0), same inputs, separate table copy
         dense = None
