@@ -1184,9 +1184,18 @@ lmscale_status lmscale_emulate_step(lmscale_ctx* const* ctxs, int world,
   for (int r = 0; r < world && !st; ++r)
     st = run_s4(ctxs[r], grads[r], s, nullptr, lr, false, cF, false, /*local_slots=*/true);
   if (st) return st;
-  // S5+S6: every rank's fused kernel (compressed: every phase 1, then every phase 2)
   char* bases[8];
   for (int j = 0; j < world; ++j) bases[j] = (char*)ctxs[j]->M;
+  // the global counts of I^ (the sparse-grad view's `counts`), from every
+  // rank's S1 counts in its window, as lmscale_sync does at world > 1
+  for (int r = 0; r < world; ++r) {
+    lmscale_ctx* c = ctxs[r];
+    CK(launch_gcounts(c->gcounts, c->ucap, c->ihat, c->sc3, nullptr, 0, c->gbits, c->wrank,
+                      (uint32_t)c->cfg.vocab, world, bases, c->lbits_off, c->lrank_off,
+                      c->counts_off, c->num_sms, s));
+    c->kernels_call += 1;
+  }
+  // S5+S6: every rank's fused kernel (compressed: every phase 1, then every phase 2)
   for (int ph = 1; ph <= (cF > 0.f ? 2 : 1); ++ph)
     for (int r = 0; r < world; ++r) {
       lmscale_ctx* c = ctxs[r];
@@ -1199,6 +1208,7 @@ lmscale_status lmscale_emulate_step(lmscale_ctx* const* ctxs, int world,
     lmscale_ctx* c = ctxs[r];
     c->have_s3 = true;
     c->m_consumed = true;
+    c->gcounts_valid = true;
     c->lbits_clean = false;
     end_call(c);
   }

@@ -120,11 +120,14 @@ def test_emulated_step_whole_table(lm, G, mode, D):
         untouched = np.setdiff1d(np.arange(cfg.V), t)
         np.testing.assert_array_equal(got[untouched], E0.cpu().numpy()[untouched])
     check_replicas(tables, f"G={G} {mode} D={D}")
-    # I^ and U_g of every rank: the sparse-grad view after the step
+    # I^, U_g and the global counts of every rank: the sparse-grad view after
+    # the step (counts summed over the peers' S1 counts read from their windows)
     for c in ctxs:
         sg = c.sparse_grad()
         assert sg.num_unique == ref["Ug"]
         np.testing.assert_array_equal(sg.ids.cpu().numpy().view(np.uint32), ref["Ihat"])
+        np.testing.assert_array_equal(sg.counts.cpu().numpy(), ref["gcounts"])
+        assert sg.rows is None  # the fused exchange consumed M
     close(ctxs)
 
 
