@@ -135,6 +135,7 @@ struct SegArgs {
   unsigned long long* trace;  // LMSCALE_PHASE_TRACE stamps (or nullptr)
   int K, D, num_sms;
   uint32_t seg_len;       // set by launch_seg: grouped positions per range
+  int fold;               // range geometry of the S1 that ran before (seg_plan)
   uint32_t vocab;         // bounds of the checked build (LMS_CHECK)
   int64_t mrows, part_rows;
   int cbw, nct, gr, nslot, neslot, lmax;
@@ -144,10 +145,12 @@ struct SegPlan {
   int cbw, nct, threads, ncb, gr, nslot, neslot, occ, nr, lmax;
   size_t smem;
 };
-SegPlan seg_plan(int64_t K, int64_t D, bool vec, bool apply, int num_sms);
+// fold: the launch geometry of the world-1 kernel with S6 folded in (else the
+// M-row geometry); S1 cuts the ranges for the S4 that follows, so both use it
+SegPlan seg_plan(int64_t K, int64_t D, bool vec, bool apply, bool fold, int num_sms);
 // the S4 ranges for (K, D): nr ranges of seg_len grouped positions (the last
 // one shorter); S1 writes runfirst for them
-int seg_ranges(int64_t K, int64_t D, int num_sms, uint32_t* seg_len);
+int seg_ranges(int64_t K, int64_t D, int num_sms, bool fold, uint32_t* seg_len);
 int64_t seg_max_ranges(int64_t K, int num_sms);
 cudaError_t launch_seg(const SegArgs& a, cudaStream_t s);
 cudaError_t launch_zero_absent(float* M, int D, const uint32_t* ihat, const uint32_t* lbits,

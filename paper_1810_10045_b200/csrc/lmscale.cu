@@ -77,6 +77,7 @@ struct lmscale_ctx {
   size_t ws_bytes = 0;
   uint32_t *luniq, *lbits, *gbits, *wrank, *I, *ihat, *ctot, *ctot1, *wcount, *tick;
   int32_t *perm, *runfirst, *inverse, *lstart, *counts, *l2g, *gcounts;
+  bool s1_fold = false;  // the S4 range geometry the last S1 cut (seg_plan's fold)
   float* part = nullptr;       // S4 partial rows of cut runs (2 nr_max x D)
   float* part2 = nullptr;      // S4 group sums of partial rows (2 nr_max x D)
   uint32_t* pcnt = nullptr;    // S4 last-arriver counters
@@ -222,8 +223,10 @@ void end_call(lmscale_ctx* c) {
 
 // S1 on stream s: one launch (counting-sort grouping over the
 // vocabulary, group.cu).  world1: I = J, so it also writes I^, l2g and U_g.
+// fold: the S4 that follows folds S6 in (world-1 step): S1 cuts the S4
+// ranges for that kernel's launch geometry (seg_plan).
 lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t* nu_out,
-                      cudaStream_t s, bool world1 = false) {
+                      cudaStream_t s, bool world1 = false, bool fold = false) {
   G1Args a;
   a.ids = ids;
   a.K = (int)k;
@@ -240,7 +243,8 @@ lmscale_status run_s1(lmscale_ctx* ctx, const uint32_t* ids, int64_t k, int64_t*
   a.perm = ctx->perm;
   a.inverse = ctx->inverse;
   a.runfirst = ctx->runfirst;
-  a.nr = seg_ranges(k, ctx->cfg.dim, ctx->num_sms, &a.seg_len);
+  a.nr = seg_ranges(k, ctx->cfg.dim, ctx->num_sms, fold, &a.seg_len);
+  ctx->s1_fold = fold;
   a.sc = ctx->sc1;
   a.nu_out = nu_out;
   a.zero_bits = ctx->lbits_clean ? 0 : 1;
@@ -365,6 +369,7 @@ lmscale_status run_s4(lmscale_ctx* ctx, const float* grad, cudaStream_t s,
   a.vocab = (uint32_t)ctx->cfg.vocab;
   a.mrows = ctx->ucap;
   a.part_rows = 2 * ctx->nr_max;
+  a.fold = ctx->s1_fold ? 1 : 0;  // the ranges S1 cut
   CK(launch_seg(a, s));
   LAUNCHED(1);
   if (world1) ctx->lbits_clean = true;
@@ -953,7 +958,7 @@ lmscale_status step_impl(lmscale_ctx* ctx, const uint32_t* ids, const float* gra
   } else {
     // world 1: I = J, so S3's I^, U_g and l2g come out of S1 (one launch).
     rec(ctx, EV_S1_BEGIN, s);
-    st = run_s1(ctx, ids, k, nullptr, s, /*world1=*/true);
+    st = run_s1(ctx, ids, k, nullptr, s, /*world1=*/true, /*fold=*/inline_s6);
     if (st) return st;
     rec(ctx, EV_S1_END, s);
     rec(ctx, EV_GATHER_END, s);

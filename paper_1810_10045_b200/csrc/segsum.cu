@@ -387,21 +387,24 @@ void seg_attrs(size_t smem) {
 }
 }  // namespace
 
-// CTAs per SM for rows of D floats (the vector path's 8 KB column blocks)
-static int seg_occ(int64_t D) {
+// CTAs per SM for rows of D floats (the vector path's 8 KB column blocks).
+// fold: the world-1 kernel with S6 folded in (E rows staged beside the
+// gradient rows); otherwise M rows are written (G > 1, staged calls).
+static int seg_occ(int64_t D, bool fold) {
   static const int occ_env = getenv("LMSCALE_S4_OCC") ? atoi(getenv("LMSCALE_S4_OCC")) : 0;
   if (occ_env > 0) return std::min(occ_env, SEG_MAX_OCC);
-  // measured best (tools/ab_s4.sh on B200): 2 KB rows 4, 4 KB rows 3, 8 KB rows 2
+  // measured best on B200: fold (tools/ab_s4.sh) 2 KB rows 4, 4 KB rows 3,
+  // 8 KB rows 2; M rows (tools/ab_seg_emu.sh) 4 / 3 / 4
   const int64_t rb = std::min<int64_t>(D, 2048) * 4;
-  return rb <= 2048 ? 4 : rb <= 4096 ? 3 : 2;
+  return rb <= 2048 ? 4 : rb <= 4096 ? 3 : fold ? 2 : 4;
 }
 
 // ranges: one per CTA of seg_occ per SM, at most SEG_MAX_L positions each,
 // at least 8 positions each; fixed length (the last one shorter), so a
 // position's range is one 32-bit division
-int seg_ranges(int64_t K, int64_t D, int num_sms, uint32_t* seg_len) {
+int seg_ranges(int64_t K, int64_t D, int num_sms, bool fold, uint32_t* seg_len) {
   const int64_t ncb = (D + 2047) / 2048;
-  const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms * seg_occ(D) / ncb);
+  const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms * seg_occ(D, fold) / ncb);
   const int64_t by_len = (K + SEG_MAX_L - 1) / SEG_MAX_L;
   const int64_t by_min = (K + 7) / 8;
   const int64_t n = std::max<int64_t>(1, std::max<int64_t>(by_len, std::min<int64_t>(cap, by_min)));
@@ -414,7 +417,7 @@ int seg_ranges(int64_t K, int64_t D, int num_sms, uint32_t* seg_len) {
 // permuted 2-8 KB rows): one CTA's bulk-copy stream saturates at 20-40 GB/s
 // whatever its ring depth, so the SM's share of HBM (~44 GB/s) needs 2-4
 // CTAs per SM with groups of 4-8 rows per mbarrier.
-SegPlan seg_plan(int64_t K, int64_t D, bool vec, bool apply, int num_sms) {
+SegPlan seg_plan(int64_t K, int64_t D, bool vec, bool apply, bool fold, int num_sms) {
   SegPlan p{};
   p.tma = vec;
   const int vw = vec ? 4 : 1;
@@ -424,14 +427,16 @@ SegPlan seg_plan(int64_t K, int64_t D, bool vec, bool apply, int num_sms) {
   p.threads = p.nct + (vec ? 32 : 0);
   p.ncb = (int)((D + p.cbw - 1) / p.cbw);
   const int rb = p.cbw * 4;
-  p.occ = seg_occ(D);
+  p.occ = seg_occ(D, fold);
   uint32_t len = 0;
-  p.nr = seg_ranges(K, D, num_sms, &len);
+  p.nr = seg_ranges(K, D, num_sms, fold, &len);
   p.lmax = (int)len;
   const size_t meta = 8 * (size_t)p.lmax;
   if (vec) {
     static const int gr_env = getenv("LMSCALE_S4_GR") ? atoi(getenv("LMSCALE_S4_GR")) : 0;
-    p.gr = gr_env > 0 ? gr_env : (rb <= 4096 ? 4 : 2);  // measured with seg_occ
+    // measured with seg_occ: fold 4 / 4 / 2 rows per group (2 / 4 / 8 KB
+    // rows), M rows 8 / 4 / 4
+    p.gr = gr_env > 0 ? gr_env : fold ? (rb <= 4096 ? 4 : 2) : (rb <= 2048 ? 8 : 4);
     const size_t budget = (size_t)(224 * 1024) / p.occ - meta - 1024;
     // a slot holds GR gradient rows and, at world 1, up to GR E rows
     // at least 2 slots, and the whole ring within one SM's shared memory
@@ -458,7 +463,7 @@ cudaError_t launch_seg(const SegArgs& a0, cudaStream_t s) {
   const bool vec = a.D % 4 == 0 && (uintptr_t)a.grad % 16 == 0 &&
                    (!a.apply || (uintptr_t)a.table % 16 == 0) &&
                    (a.apply || (uintptr_t)a.M % 16 == 0) && (uintptr_t)a.part % 16 == 0;
-  const SegPlan p = seg_plan(a.K, a.D, vec, a.apply != 0, a.num_sms);
+  const SegPlan p = seg_plan(a.K, a.D, vec, a.apply != 0, a.fold != 0, a.num_sms);
   a.cbw = p.cbw;
   a.nct = p.nct;
   a.gr = p.gr;
