@@ -25,6 +25,10 @@ grads = [synth.grad_values(cfg.K, cfg.D, "signed", rank=r, device=dev) for r in 
 tables = [synth.table_values(cfg.V, cfg.D, "signed", device=dev) for _ in range(G)]
 ctxs = [lmscale.Context(cfg.V, cfg.K, cfg.D, world=G, rank=r, flags=lmscale.FLAG_NO_COMM)
         for r in range(G)]
+F = float(os.environ.get("EMU_COMPRESS", "0"))   # Sec. 3.3 compressed exchange (binary16 M rows)
+if F > 0:
+    for c in ctxs:
+        c.set_compression(F)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for s in range(steps):
     torch.cuda.synchronize()
