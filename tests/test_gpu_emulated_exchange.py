@@ -351,3 +351,44 @@ def test_emulated_seeded_output_exchange(lm, policy):
     check_replicas(tables, f"seeded {policy}")
     assert ctxs[0].sparse_grad().num_unique == ref["Ug"]
     close(ctxs)
+
+
+def _random_cases(n=24, seed=18101004):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        G = int(rng.integers(2, 9))
+        V = int(rng.choice([1, 2, 31, 33, 1000, 40000]))
+        K = int(rng.choice([1, 2, 7, 300, 2049, 5000]))
+        D = int(rng.choice([1, 3, 4, 17, 64, 100, 512, 516]))
+        s = float(rng.choice([0.5, 1.0, 1.5]))
+        cases.append((i, G, V, K, D, s))
+    return cases
+
+
+@pytest.mark.parametrize("i,G,V,K,D,s", _random_cases(),
+                         ids=[f"case{c[0]}-G{c[1]}-V{c[2]}-K{c[3]}-D{c[4]}-s{c[5]}" for c in _random_cases()])
+def test_emulated_random_shapes(lm, i, G, V, K, D, s):
+    """Seeded random shapes for the world-G step (vocab 1..40000 incl. one
+    bitmap word and its edge, K from 1 token, D from 1 float, the vector and
+    the scalar kernels, flat to steep Zipf): INT mode, every replica's whole
+    table bit-exact against oracle.sync_unique, I^ and the global counts too."""
+    cfg = synth.Config("rand", V=V, K=K, D=D, G=G, s=s)
+    lr = synth.default_lr("int")
+    J = [synth.zipf_ids(V, s, K, rank=g, step=i) for g in range(G)]
+    Dl = [synth.grad_values(K, D, "int", rank=g, step=i) for g in range(G)]
+    E0 = synth.table_values(V, D, "int", device=dev())
+    tables = [E0.clone() for _ in range(G)]
+    ctxs = make(lm, cfg, G)
+    lm.emulate_step(ctxs, [ids_dev(j) for j in J], [d.to(dev()) for d in Dl], tables, lr)
+    torch.cuda.synchronize()
+    Eo = E0.cpu().numpy().copy()
+    ref = oracle.sync_unique(J, [d.numpy() for d in Dl], Eo, lr)
+    np.testing.assert_array_equal(tables[0].cpu().numpy(), Eo)
+    check_replicas(tables, f"random case {i}")
+    for c in ctxs:
+        sg = c.sparse_grad()
+        assert sg.num_unique == ref["Ug"]
+        np.testing.assert_array_equal(sg.ids.cpu().numpy().view(np.uint32), ref["Ihat"])
+        np.testing.assert_array_equal(sg.counts.cpu().numpy(), ref["gcounts"])
+    close(ctxs)

@@ -237,3 +237,40 @@ def test_id_range_error_leaves_everything_untouched(lm):
     oracle.sync_unique([J], [g.cpu().numpy()], Eo, 0.5)
     np.testing.assert_array_equal(E.cpu().numpy(), Eo)
     ctx.close()
+
+
+def _random_w1(n=24, seed=18101005):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        out.append((i, int(rng.choice([1, 2, 31, 33, 1000, 40000, 300000])),
+                    int(rng.choice([1, 2, 7, 300, 2049, 5000, 70000])),
+                    int(rng.choice([1, 3, 4, 17, 64, 100, 512, 516, 2048])),
+                    float(rng.choice([0.5, 1.0, 1.5])), bool(rng.integers(0, 2))))
+    return out
+
+
+@pytest.mark.parametrize("i,V,K,D,s,graph", _random_w1(),
+                         ids=[f"case{c[0]}-V{c[1]}-K{c[2]}-D{c[3]}-s{c[4]}-{'graph' if c[5] else 'eager'}"
+                              for c in _random_w1()])
+def test_world1_step_random_shapes(lm, i, V, K, D, s, graph):
+    """Seeded random shapes for the world-1 step (S1 + S4 with S6 folded;
+    the scalar kernel for dim % 4 != 0; vocab from 1 id; K from 1 token;
+    ranges cut inside runs of every length), eager or CUDA-graph replay,
+    INT mode: the whole table bit-exact against the oracle's steps 1-7."""
+    lr = synth.default_lr("int")
+    J = synth.zipf_ids(V, s, K, step=i)
+    g = synth.grad_values(K, D, "int", step=i)
+    E0 = synth.table_values(V, D, "int", device=dev())
+    E = E0.clone()
+    ctx = lm.Context(V, K, D, flags=lm.FLAG_GRAPH if graph else 0)
+    ids = torch.from_numpy(J.view(np.int32)).to(dev())
+    gd = g.to(dev())
+    for _ in range(2):
+        ctx.step(ids, gd, E, lr)
+    torch.cuda.synchronize()
+    Eo = E0.cpu().numpy().copy()
+    for _ in range(2):
+        oracle.sync_unique([J], [g.numpy()], Eo, lr)
+    np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+    ctx.close()
