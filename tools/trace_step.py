@@ -15,6 +15,8 @@ from paper_1810_10045_b200 import lmscale  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "1b"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 cfg = synth.CONFIGS[name]
+if os.environ.get("TRACE_S"):   # Zipf exponent override
+    cfg = cfg.with_(s=float(os.environ["TRACE_S"]))
 dev = torch.device("cuda", 0)
 ids = torch.from_numpy(synth.ids_for(cfg, 0).view(np.int32)).to(dev)
 grad = synth.grad_values(cfg.K, cfg.D, "signed", device=dev)
