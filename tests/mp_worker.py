@@ -396,6 +396,42 @@ def run_compressed_discriminating(rank, G, dev):
     ctx.close()
 
 
+def run_long(cfg, rank, G, dev, steps=200, comp=False):
+    """Many CUDA-graph replays of the benched path (table window, P2P fused
+    S5+S6, S4 beside the peer-bitmap S3 -- or the compressed exchange) with a
+    new batch every step (ids and gradients copied into the captured
+    buffers): the flag handshake epochs, the LSA barriers and the presence
+    bitmaps are exercised `steps` times; INT mode, the final table bit-exact
+    against the oracle applying the same `steps` exchanges in order."""
+    mode = "int"
+    lr = synth.default_lr(mode)
+    ctx = make_context(cfg.V, cfg.K, cfg.D, flags=lmscale.FLAG_GRAPH)
+    if comp:
+        ctx.set_compression(1.0)
+    E = ctx.alloc_table()
+    E0 = synth.table_values(cfg.V, cfg.D, mode)
+    E.copy_(E0.to(dev))
+    ids = torch.empty(cfg.K, dtype=torch.int32, device=dev)
+    grad = torch.empty(cfg.K, cfg.D, dtype=torch.float32, device=dev)
+    Eo = E0.numpy().copy()
+    for s in range(steps):
+        J = [synth.ids_for(cfg, g, step=s) for g in range(G)]
+        Dl = [synth.grad_values(cfg.K, cfg.D, mode, rank=g, step=s) for g in range(G)]
+        ids.copy_(torch.from_numpy(J[rank].view(np.int32)))
+        grad.copy_(Dl[rank])
+        ctx.step(ids, grad, E, lr)
+        if comp:
+            oracle.sync_unique_compressed(J, [d.numpy() for d in Dl], Eo, lr, 1.0)
+        else:
+            oracle.sync_unique(J, [d.numpy() for d in Dl], Eo, lr)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(E.cpu().numpy(), Eo)
+    check_replicas(E, f"long {cfg.name} comp={comp}")
+    if rank == 0:
+        print(f"long G={G} {cfg.name} {steps} graph-replayed steps comp={comp}: bit-exact", flush=True)
+    ctx.close()
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -434,6 +470,10 @@ def main():
         run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "int", rank, G, dev, 1.0, fmt="bf16")
         run_compressed_small(synth.CONFIGS["tiny"].with_(G=G), "signed", rank, G, dev, 1.0,
                              own_table=True, fmt="bf16")
+    if "long" in which:
+        cfg = synth.Config("long", V=50000, K=8192, D=128, G=G)
+        run_long(cfg, rank, G, dev, steps=200)
+        run_long(cfg, rank, G, dev, steps=100, comp=True)
     if "p2p" in which:
         # the launch configuration bench.py times (table window, P2P fused
         # S5+S6), fp32 and compressed, at 1b and tieba full size
