@@ -169,12 +169,16 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
 // acquire once after the loop.  (An acquire load per poll and a reset store
 // before the release left ~2.2 us between the last arrival and the others
 // passing.)
+// gen is loaded BEFORE the CTA's __syncthreads, so its round trip overlaps
+// the wait for the CTA's other warps: it cannot change before this CTA
+// arrives, and thread 0 has already seen the previous release (coherence).
 __device__ __forceinline__ void grid_barrier(GridBar* b) {
+  uint32_t gen = 0;
+  if (threadIdx.x == 0)
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(&b->gen) : "memory");
   __syncthreads();  // the CTA's writes happen-before thread 0's release below
   if (threadIdx.x == 0) {
     const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
-    uint32_t gen;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(&b->gen) : "memory");
     uint32_t old;
     asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;"
                  : "=r"(old) : "l"(&b->count), "r"(nb - 1u) : "memory");

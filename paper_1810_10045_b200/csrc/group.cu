@@ -276,6 +276,11 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     // (the counts are returned to zero right after they are read, once per
     // id -- zeroing them per token in PD queued thousands of stores on the
     // Zipf head's counters: 15 us at tieba)
+    // The tile holds, per (bit i, word), the INCLUSIVE prefix of the word's
+    // counts over bits 0..i, summed by the word's lane in registers: the
+    // emission below reads a run's start and count from two tile entries
+    // instead of a per-word warp scan (its shuffle chain serialised the
+    // words: ~3 us of the Zipf head's ranges at 1b).
     auto load_chunk = [&](int64_t xc, uint32_t& mybits, bool zero) -> uint32_t {
       const int64_t myw = xc + lane;
       mybits = myw < x1 ? __ldcg(a.lbits + myw) : 0u;
@@ -290,18 +295,19 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        tile[i * 33 + lane] = v[i];
         tot += v[i];
+        tile[i * 33 + lane] = tot;
       }
       __syncwarp();
       return tot;  // this lane's word total
     };
     // pass 1: this warp's totals
-    uint32_t wu = 0, wt = 0, bits0 = 0;
+    uint32_t wu = 0, wt = 0, bits0 = 0, tot0 = 0;
     const bool one_chunk = x1 - x0 <= 32;
     for (int64_t xc = x0; xc < x1; xc += 32) {
       uint32_t mybits;
-      wt += load_chunk(xc, mybits, one_chunk);
+      tot0 = load_chunk(xc, mybits, one_chunk);
+      wt += tot0;
       wu += __popc(mybits);
       bits0 = mybits;
       __syncwarp();
@@ -318,36 +324,43 @@ __global__ void __launch_bounds__(G1_THREADS, 1) k_group(G1Args a) {
     gstamp(a.trace, 9);
     // pass 2: emit J^, counts, lstart, lrank (lane = bit: coalesced stores)
     for (int64_t xc = x0; xc < x1; xc += 32) {
-      uint32_t mybits = bits0;
-      if (!one_chunk) load_chunk(xc, mybits, true);
+      uint32_t mybits = bits0, mytot = tot0;
+      if (!one_chunk) mytot = load_chunk(xc, mybits, true);
+      // per-word bases (lane = word): exclusive scans of ids and tokens
+      uint32_t su = __popc(mybits), stt = mytot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yu = __shfl_up_sync(FULL, su, o), yt = __shfl_up_sync(FULL, stt, o);
+        if (lane >= o) {
+          su += yu;
+          stt += yt;
+        }
+      }
+      const uint32_t wbu = bu + su - __popc(mybits), wbt = bt + stt - mytot;
       const int nwc = (int)(x1 - xc < 32 ? x1 - xc : 32);
       for (int j = 0; j < nwc; ++j) {
         const int64_t w = xc + j;
         const uint32_t bits = __shfl_sync(FULL, mybits, j);
+        const uint32_t ubase = __shfl_sync(FULL, wbu, j), tbase = __shfl_sync(FULL, wbt, j);
         const bool has = (bits >> lane) & 1u;
-        const uint32_t cnt = tile[lane * 33 + j];
-        uint32_t inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(FULL, inc, o);
-          if (lane >= o) inc += y;
-        }
-        if (lane == 0) a.lrank[w] = bu;
+        const uint32_t inc = tile[lane * 33 + j];
+        const uint32_t exc = lane ? tile[(lane - 1) * 33 + j] : 0u;
+        if (lane == 0) a.lrank[w] = ubase;
         if (has) {
           const uint32_t id = (uint32_t)(w * 32 + lane);
-          const uint32_t u = bu + __popc(bits & lanemask_lt());
-          LMS_CHECK(u < (uint32_t)a.K && bt + inc <= (uint32_t)a.K && id < a.vocab);
+          const uint32_t u = ubase + __popc(bits & lanemask_lt());
+          LMS_CHECK(u < (uint32_t)a.K && tbase + inc <= (uint32_t)a.K && id < a.vocab);
           a.luniq[u] = id;
-          a.counts[u] = (int32_t)cnt;
-          a.lstart[u] = (int32_t)(bt + inc - cnt);
+          a.counts[u] = (int32_t)(inc - exc);
+          a.lstart[u] = (int32_t)(tbase + exc);
           if (a.ihat) {
             a.ihat[u] = id;
             a.l2g[u] = (int32_t)u;
           }
         }
-        bu += __popc(bits);
-        bt += __shfl_sync(FULL, inc, 31);
       }
+      bu += __shfl_sync(FULL, su, 31);
+      bt += __shfl_sync(FULL, stt, 31);
       __syncwarp();
     }
     // the last range ends at U_i (ids) and the valid token count
