@@ -2,6 +2,8 @@
 # A/B of the early programmatic trigger of the world-1 S4 at small K:
 # alternating bench lines (1b, 50 steps) with and without it, phase traces,
 # and the world-1 step parity tests -> gpurun_out/trig/
+# (historical: the LMSCALE_NO_EARLY_TRIGGER switch and the trigger itself were
+# removed after this A/B showed no gain -- DESIGN.md, rejected table)
 mkdir -p gpurun_out/trig
 for rep in 1 2 3; do
   for tag in on off; do
